@@ -1,0 +1,276 @@
+/*
+ * expkit_sm100.h — C ABI of libexpkit_sm100.so, the B200 (sm_100a) engine for
+ * the phi-action hot path of arXiv 2211.08948 (reference: /root/reference,
+ * package `expkit`).
+ *
+ * Plain C: pointers, sizes, POD structs. No torch types. All `double*`
+ * vector arguments are DEVICE pointers (fp64, contiguous) unless the name
+ * ends in `_host`. Every entry point takes the CUDA stream it must run on
+ * (`void* stream`, a cudaStream_t; NULL = legacy default stream) and returns
+ * an int status (EK_OK = 0); `ek_last_error()` gives the text of the last
+ * failure on the calling thread.
+ *
+ * Each function names the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/expkit/). INTEGRATION.md shows the ctypes binding a
+ * reference maintainer would add.
+ *
+ * Numerics: compiled with -fmad=false (no FMA contraction) and IEEE division,
+ * so elementwise arithmetic follows NumPy's operation order bit-for-bit
+ * (SURVEY.md §8(a)). Reductions are deterministic: fixed block partials,
+ * reduced in a fixed order by the last block to finish (run-to-run and
+ * scheduling invariant).
+ */
+#ifndef EXPKIT_SM100_H
+#define EXPKIT_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+#define EK_OK 0
+#define EK_ERR_INVALID 1      /* bad argument (-> ValueError)                */
+#define EK_ERR_CUDA 2         /* CUDA runtime failure                        */
+#define EK_ERR_UNSUPPORTED 3  /* combination not implemented                 */
+
+/* device-side numerical status codes (ek_*_state.status) */
+#define EK_ST_OK 0
+#define EK_ST_JV_NONFINITE 1   /* non-finite FD Jacobian action: linalg.py:127-128 -> FloatingPointError */
+#define EK_ST_NORM_NONFINITE 2 /* non-finite ||y||: leja.py:173-175 -> NonConvergence               */
+#define EK_ST_REM_NONFINITE 3  /* non-finite remainder: integrators.py:107-108 -> FloatingPointError */
+
+/* ------------------------------------------------------------------ grids */
+enum ek_problem {
+    EK_P_ADR = 1,             /* problems.py:69-83                         */
+    EK_P_ALLEN_CAHN = 2,      /* problems.py:86-97 (+ periodic variant)    */
+    EK_P_BRUSS_PRINTED = 3,   /* problems.py:100-124, form="printed"       */
+    EK_P_BRUSS_STANDARD = 4,  /* problems.py:100-124, form="standard"      */
+    EK_P_GRAY_SCOTT = 5,      /* problems.py:127-145                       */
+    EK_P_SEMILINEAR = 6,      /* problems.py:154-196 (1-D, nonlocal term)  */
+    EK_P_ADVDIFF2D = 7,       /* BASELINE config 1 (not in the reference)  */
+    EK_P_BURGERS2D = 8,       /* BASELINE config 3 (not in the reference)  */
+    EK_P_ADVDIFF3D = 9        /* BASELINE config 5 (not in the reference)  */
+};
+enum ek_bc { EK_BC_NEUMANN = 0, EK_BC_PERIODIC = 1, EK_BC_DIRICHLET = 2 };
+enum ek_jac { EK_JAC_FD = 0, EK_JAC_ANALYTIC = 1 };
+
+/* Uniform grid of one problem, component-major vectors with flat index
+ * i*n + j (2-D, i = x slowest, problems.py meshgrid indexing="ij") or
+ * (i*n + j)*n + k (3-D). For slab decomposition (multi-GPU) the local vector
+ * holds rows [row0, row0+rows) of axis 0 and the rows just outside come from
+ * halo buffers; single-GPU: rows == n, row0 == 0, slab == 0. */
+typedef struct ek_grid {
+    int32_t problem;   /* enum ek_problem                                  */
+    int32_t bc;        /* enum ek_bc                                       */
+    int32_t dim;       /* 1, 2 or 3                                        */
+    int32_t ncomp;     /* 1 or 2 components                                */
+    int64_t n;         /* points per axis                                  */
+    int64_t rows;      /* local extent of axis 0                           */
+    int64_t row0;      /* global index of local row 0                      */
+    int32_t slab;      /* 1: rows -1 and `rows` come from halo buffers     */
+    int32_t pad_;
+    double h;          /* grid spacing                                     */
+    double h2;         /* h**2 exactly as Python evaluates it              */
+    double two_h;      /* 2.0*h                                            */
+    double prm[8];     /* problem parameters            */
+} ek_grid;
+
+/* Length of one state vector (ncomp * points, +1 for the semilinear time). */
+int64_t ek_grid_len(const ek_grid* g);
+
+/* -------------------------------------------------------- device states */
+/* Leja iteration control block, lives in device memory (leja.py:159-184).
+ * The host initialises tol, nu, k (and zeroes the rest) before
+ * ek_leja_begin_len. */
+typedef struct ek_leja_state {
+    double ny;          /* ||y_m|| of the last finalised iterate            */
+    double eps;         /* FD increment for the next Jacobian action        */
+    double nu;          /* ||u|| at the linearisation point                 */
+    double tol;         /* absolute termination tolerance                   */
+    int32_t m;          /* index of the last finalised iterate              */
+    int32_t done;       /* 1: all accumulators frozen, or an error          */
+    int32_t status;     /* EK_ST_*                                          */
+    int32_t k;          /* number of accumulators (<= 8)                    */
+    uint32_t active;    /* bit i: accumulator i still accumulating          */
+    int32_t fd_evals;   /* FD Jacobian actions performed (RHS charges)      */
+    uint32_t ticket;    /* internal: last-block counter (keep 0)            */
+    int32_t iters;      /* iteration count at termination                   */
+    int32_t freeze[8];  /* freeze_iters                                     */
+} ek_leja_state;
+
+/* Scalar reduction slot (norms, dots, flags), device memory. */
+typedef struct ek_scalar_state {
+    double val[8];      /* reduced values                                   */
+    int32_t flag;       /* bit0: any nonzero, bit1: any non-finite          */
+    uint32_t ticket;    /* internal (keep 0)                                */
+    int32_t count;
+    int32_t status;     /* EK_ST_*                                          */
+} ek_scalar_state;
+
+/* Power iteration control block (spectrum.py:43-63). Host initialises
+ * lam = 0, nu, tol_pi, max_it. */
+typedef struct ek_power_state {
+    double lam;         /* last estimate                                    */
+    double nw;          /* ||J v|| of the last iteration (next divisor)     */
+    double nv;          /* ||v|| of the current iterate (FD increment)      */
+    double nu;          /* ||u||                                            */
+    double tol_pi;
+    int32_t it;         /* iterations done                                  */
+    int32_t max_it;
+    int32_t done;
+    int32_t converged;
+    int32_t fd_evals;
+    uint32_t ticket;    /* internal (keep 0)                                */
+    int32_t status;     /* EK_ST_*                                          */
+    int32_t pad_;
+} ek_power_state;
+
+/* KIOPS Arnoldi control block (kiops.py:168-194). Host initialises nu, tol. */
+typedef struct ek_arnoldi_state {
+    double nrm;         /* last ||w|| (and the current normaliser)          */
+    double nvn;         /* ||V[j,:n]|| (FD increment of the next Jv)        */
+    double nu;          /* ||u||                                            */
+    double tol;         /* happy-breakdown threshold                        */
+    double beta;        /* ||V[0]|| of the current substep                  */
+    int32_t j;          /* current basis size                               */
+    int32_t happy;      /* 1 = happy breakdown                              */
+    int32_t status;     /* EK_ST_*                                          */
+    int32_t fd_evals;   /* FD Jacobian actions performed                    */
+    uint32_t ticket;    /* internal (keep 0)                                */
+    int32_t pad_;
+} ek_arnoldi_state;
+
+/* ------------------------------------------------------------ utilities */
+const char* ek_last_error(void);
+int ek_version(void);
+/* Bytes of device workspace (block partials) any call on this grid needs. */
+int64_t ek_workspace_bytes(const ek_grid* g);
+/* Stream-ordered copies (kind: 1 = host->device, 2 = device->host; a copy
+ * to pageable host memory returns after the stream reached it). */
+int ek_copy(void* dst, const void* src, int64_t bytes, int kind, void* stream);
+int ek_sync(void* stream);
+
+/* ------------------------------------------------ stencils (problems.py) */
+/* out = f(u). Replaces Problem.rhs closures, problems.py:76-80, 92-95,
+ * 115-121, 136-142, 170-175 (+ BASELINE plugins). halo: NULL, or
+ * {u_halo, y_halo, k_halo} for a slab. */
+int ek_rhs(const ek_grid* g, const double* u, double* out,
+           const double* const* halo, void* stream);
+
+/* out = J(u) v.  jac = EK_JAC_FD: (f(u+eps v) - fu)/eps with the caller's
+ * eps = (sqrt(eps_mach)*(1+||u||))/||v|| (linalg.py:111-129); when `st` is
+ * given, st->flag bit1 reports a non-finite result (linalg.py:127-128).
+ * jac = EK_JAC_ANALYTIC: the problem's exact Jacobian stencil
+ * (problems.py:177-189 / BASELINE plugins). */
+int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu,
+          const double* v, double eps, double* out, ek_scalar_state* st,
+          double* work, const double* const* halo, void* stream);
+
+/* Fused nonlinear remainder R(k) = (f(k) - f_n) - J(k-u), one HBM pass over
+ * both stencils (integrators.py:99-109). FD: J(dk) = (f(u+eps dk)-f_n)/eps
+ * with the caller's eps from ||k-u||. st->flag bit1: non-finite output. */
+int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu,
+                 const double* k, double eps, double* out, ek_scalar_state* st,
+                 double* work, void* stream);
+
+/* ------------------------------------------------------- Leja (leja.py) */
+/* Coefficient table coef_dev: (k+1) rows x 32 columns, row 0 the shifts
+ * c/gamma + xi[m-1], row 1+i the divided differences d_i[m], column
+ * m - chunk_base. */
+
+/* m = 0 of leja_interpolate_vertical (leja.py:159-165): p_i = d_i[0]*b,
+ * ||b||, freeze test, FD increment for m = 1. */
+int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
+                      const double* coef_dev, ek_leja_state* st, double* work,
+                      void* stream);
+
+/* Iterations m in [m_begin, m_end) of the Newton-Leja recurrence
+ * (leja.py:167-184), each ONE fused HBM pass: Jacobian stencil (FD or
+ * analytic) + y' = Jy/gamma - shift*y + p_i += d_i[m] y' + deterministic
+ * ||y'||^2 + device-side freeze test. y ping-pongs between ybuf[0]/ybuf[1];
+ * iterate m-1 is read from `b` when m == 1. Launches early-exit once
+ * st->done is set, so the host syncs only per chunk. */
+int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu,
+                const double* b, double* const* ybuf, double* const* p, int k,
+                const double* coef_dev, int chunk_base, int m_begin, int m_end,
+                double gamma, ek_leja_state* st, double* work, void* stream);
+
+/* One recurrence step for a Jacobian action computed elsewhere (dense,
+ * callable or 1-D operators): y' = jv/gamma - shift*y, accumulators, norm,
+ * freeze test (leja.py:172-184). */
+int ek_leja_update(int64_t len, const double* jv, const double* y,
+                   double* ynext, double* const* p, int k,
+                   const double* coef_dev, int chunk_base, int m,
+                   double gamma, int check_jv, ek_leja_state* st,
+                   double* work, void* stream);
+
+/* ------------------------------------------------ spectrum (spectrum.py) */
+/* Power iterations it in [it_begin, it_end) (spectrum.py:43-63) on a native
+ * stencil Jacobian, no host sync: it_begin == 0 first normalises v0
+ * (spectrum.py:50-51); the iterate is read as w/||w|| (scaled on read, bit-
+ * identical to the reference's v = w / nw). Output ping-pongs in wbuf. */
+int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu,
+                 const double* v0, double* const* wbuf, int it_begin,
+                 int it_end, ek_power_state* st, double* work, void* stream);
+
+/* --------------------------------------------------- KIOPS (kiops.py) */
+/* V[0] = [src ; tail], beta = ||V[0]||, V[0] /= beta, ||V[0,:n]||
+ * (kiops.py:168-177). Rows of V are device pointers of length n+p. */
+int ek_arnoldi_init(int64_t n, int p, const double* src, const double* tail_host,
+                    double* V0, ek_arnoldi_state* st, double* work, void* stream);
+
+/* Arnoldi steps j_begin+1 .. j_end (kiops.py:180-194) on a native stencil
+ * operator A = dt*J: pass A fuses Jv + augmentation tail@u_flip (the
+ * nonzero rows of u_flip are passed as aug[t] = u_flip row / aug_scale with
+ * the tail index aug_tail[t] they multiply) + window dots; pass B the CGS subtraction +
+ * norm + happy test; pass C the normalisation + ||V[j,:n]||. H is a device
+ * row-major ldh x ldh matrix. Stops (early-exit) at a happy breakdown. */
+int ek_arnoldi_run(const ek_grid* g, int jac, const double* u,
+                   const double* fu, double* const* V, const double* const* aug,
+                   const int* aug_tail, int naug, double aug_scale,
+                   int j_begin, int j_end,
+                   double* H, ek_arnoldi_state* st, int p, int iop, int ldh,
+                   double dt, double* work, void* stream);
+
+/* Generic-operator Arnoldi: pass A with the (already scaled) action jv. */
+int ek_arnoldi_augment(int64_t n, int p, const double* jv, double* const* V,
+                       int jj, int iop, const double* const* aug,
+                       const int* aug_tail, int naug, double aug_scale,
+                       double* H, int ldh,
+                       ek_arnoldi_state* st, double* work, void* stream);
+/* Passes B and C for basis vector jj. */
+int ek_arnoldi_orth(int64_t n, int p, double* const* V, int jj, int iop,
+                    double* H, int ldh, ek_arnoldi_state* st, double* work,
+                    void* stream);
+
+/* out = sum_i coef_host[i] * V[i][:n], i < j  (kiops.py:267, 270). */
+int ek_basis_combine(int64_t n, double* const* V, const double* coef_host,
+                     int j, double* out, void* stream);
+
+/* ------------------------------------------------------------ vectors */
+/* Elementwise stack program over up to 8 inputs / 4 outputs, NumPy
+ * operation order (stage algebra of integrators.py:258-416). Opcodes:
+ * 1 LOAD i, 2 CONST s, 3 ADD, 4 SUB, 5 MUL, 6 DIV, 7 NEG, 8 STORE o, 9 POP,
+ * 10 NORM slot (st->val[0|2] = ssq, val[1|3] = sqrt), 11 CHECK (flags);
+ * word = op | arg << 8. */
+int ek_vexpr(int64_t len, const int32_t* prog, int nprog,
+             const double* scal, int nscal, const double* const* in, int nin,
+             double* const* out, int nout, ek_scalar_state* st, double* work,
+             void* stream);
+/* ||x||^2 -> st->val[slot], ||x|| -> st->val[slot+1]; st->flag bit0 any
+ * nonzero, bit1 any non-finite. */
+int ek_norm2(int64_t len, const double* x, ek_scalar_state* st, int slot,
+             double* work, void* stream);
+/* sum |x| -> st->val[slot]  (kiops.py:146). */
+int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot,
+          double* work, void* stream);
+/* y = A x, A dense row-major (linalg.py:87-90 from_matrix). */
+int ek_dense_gemv(int64_t n, const double* A, const double* x, double* y,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXPKIT_SM100_H */

@@ -1,0 +1,279 @@
+"""Device plumbing: fp64 CUDA tensors (torch = allocator + streams only),
+device state blocks, workspaces, and the elementwise-expression builder that
+lowers NumPy-style stage algebra to one `ek_vexpr` launch.
+
+Every computation below runs in libexpkit_sm100.so on the current CUDA
+device; torch is used for memory, streams and host<->device copies.
+"""
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+F64 = torch.float64
+
+
+# ---------------------------------------------------------------- device
+
+def device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2211_08948_b200 needs a CUDA device (B200); "
+                           "there is no CPU fallback")
+    N.lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def is_dev(x):
+    return isinstance(x, torch.Tensor)
+
+
+def to_dev(x, copy=False):
+    """fp64 contiguous 1-D CUDA tensor view/copy of x (numpy or torch)."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device(), dtype=F64)
+        t = t.contiguous().reshape(-1)
+        if copy and t.data_ptr() == x.data_ptr():
+            t = t.clone()
+        return t
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64)).reshape(-1)
+    return torch.from_numpy(arr).to(device=device())
+
+
+def like_input(t, ref):
+    """Return t in the kind of `ref`: numpy in -> numpy out, tensor -> tensor."""
+    if isinstance(ref, torch.Tensor):
+        return t
+    return t.cpu().numpy()
+
+
+def to_host(t):
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def empty(n):
+    return torch.empty(int(n), dtype=F64, device=device())
+
+
+def zeros(n):
+    return torch.zeros(int(n), dtype=F64, device=device())
+
+
+# ------------------------------------------------------------- workspace
+
+_WORK = {}
+
+
+def work(nbytes=None):
+    """Per-device scratch for block partials (grows monotonically)."""
+    dev = torch.cuda.current_device()
+    need = max(int(nbytes or 0), 148 * 16 * 8 * 8)
+    buf = _WORK.get(dev)
+    if buf is None or buf.numel() * 8 < need:
+        buf = torch.empty((need + 7) // 8, dtype=F64, device=device())
+        _WORK[dev] = buf
+    return buf
+
+
+def work_ptr(nbytes=None):
+    return C.c_void_p(work(nbytes).data_ptr())
+
+
+# ---------------------------------------------------------- state blocks
+
+class DevState:
+    """A ctypes Structure mirrored in device memory."""
+
+    def __init__(self, ctype, **init):
+        self.ctype = ctype
+        self.size = C.sizeof(ctype)
+        self.buf = torch.zeros(self.size, dtype=torch.uint8, device=device())
+        self.host = ctype()
+        for k, v in init.items():
+            setattr(self.host, k, v)
+        self.upload()
+
+    @property
+    def ptr(self):
+        return C.c_void_p(self.buf.data_ptr())
+
+    def upload(self):
+        N.check(N.lib().ek_copy(self.ptr, C.byref(self.host), self.size, 1, stream()),
+                "state upload")
+
+    def read(self):
+        """Stream-ordered D2H copy into pageable memory: returns once the
+        stream has reached this point (the host sync of a chunk)."""
+        N.check(N.lib().ek_copy(C.byref(self.host), self.ptr, self.size, 2, stream()),
+                "state read")
+        return self.host
+
+
+def scalar_state():
+    return DevState(N.ScalarState)
+
+
+def norm2(x, st=None):
+    """(||x||, flags) of a device vector; synchronises. flags bit0: any
+    nonzero, bit1: any non-finite."""
+    st = st or scalar_state()
+    N.check(N.lib().ek_norm2(x.numel(), C.c_void_p(x.data_ptr()), st.ptr, 0,
+                             work_ptr(), stream()), "ek_norm2")
+    h = st.read()
+    return float(h.val[1]), int(h.flag)
+
+
+def l1(x):
+    st = scalar_state()
+    N.check(N.lib().ek_l1(x.numel(), C.c_void_p(x.data_ptr()), st.ptr, 0,
+                          work_ptr(), stream()), "ek_l1")
+    return float(st.read().val[0])
+
+
+# ------------------------------------------------------- vexpr builder
+
+class Expr:
+    """Tiny expression tree mirroring NumPy elementwise evaluation order.
+
+    Python builds `w3a * Ra + w3b * Rb` with the same associativity for Expr
+    leaves as it does for numpy arrays, so compiling the tree to the stack
+    program gives the reference's rounding sequence exactly."""
+
+    __slots__ = ("op", "a", "b")
+    __array_priority__ = 1000
+
+    def __init__(self, op, a=None, b=None):
+        self.op, self.a, self.b = op, a, b
+
+    @staticmethod
+    def wrap(x):
+        if isinstance(x, Expr):
+            return x
+        if isinstance(x, torch.Tensor):
+            return Expr("vec", x)
+        if isinstance(x, (float, int, np.floating, np.integer)):
+            return Expr("const", float(x))
+        raise TypeError(f"unsupported operand {type(x)}")
+
+    def __add__(self, o): return Expr("add", self, Expr.wrap(o))
+    def __radd__(self, o): return Expr("add", Expr.wrap(o), self)
+    def __sub__(self, o): return Expr("sub", self, Expr.wrap(o))
+    def __rsub__(self, o): return Expr("sub", Expr.wrap(o), self)
+    def __mul__(self, o): return Expr("mul", self, Expr.wrap(o))
+    def __rmul__(self, o): return Expr("mul", Expr.wrap(o), self)
+    def __truediv__(self, o): return Expr("div", self, Expr.wrap(o))
+    def __rtruediv__(self, o): return Expr("div", Expr.wrap(o), self)
+    def __neg__(self): return Expr("neg", self)
+
+
+def V(t):
+    """Leaf for a device vector."""
+    return Expr("vec", t)
+
+
+_OPC = {"add": N.VX_ADD, "sub": N.VX_SUB, "mul": N.VX_MUL, "div": N.VX_DIV}
+
+
+class _Prog:
+    def __init__(self):
+        self.code, self.scal, self.ins = [], [], []
+
+    def emit(self, op, arg=0):
+        self.code.append(op | (arg << 8))
+
+    def vec(self, t):
+        for i, x in enumerate(self.ins):
+            if x.data_ptr() == t.data_ptr() and x.numel() == t.numel():
+                return i
+        self.ins.append(t)
+        return len(self.ins) - 1
+
+    def const(self, v):
+        self.scal.append(float(v))
+        return len(self.scal) - 1
+
+    def lower(self, e):
+        if e.op == "vec":
+            self.emit(N.VX_LOAD, self.vec(e.a))
+        elif e.op == "const":
+            self.emit(N.VX_CONST, self.const(e.a))
+        elif e.op == "neg":
+            self.lower(e.a)
+            self.emit(N.VX_NEG)
+        else:
+            self.lower(e.a)
+            self.lower(e.b)
+            self.emit(_OPC[e.op])
+
+
+def evaluate(outputs, length, norm=False, check=False):
+    """Run one fused elementwise pass.
+
+    outputs: list of (Expr, out_tensor_or_None). norm/check apply to the
+    first expression: returns (||value||, flags) after a sync when either
+    is requested, else None."""
+    pr = _Prog()
+    outs = []
+    for i, (ex, out) in enumerate(outputs):
+        pr.lower(Expr.wrap(ex))
+        if out is not None:
+            outs.append(out)
+            pr.emit(N.VX_STORE, len(outs) - 1)
+        if i == 0 and norm:
+            pr.emit(N.VX_NORM, 0)
+        if i == 0 and check:
+            pr.emit(N.VX_CHECK)
+        pr.emit(N.VX_POP)
+    if len(pr.ins) > 8 or len(pr.scal) > 16 or len(pr.code) > 48:
+        raise ValueError("elementwise program too large")
+    code = (C.c_int32 * len(pr.code))(*pr.code)
+    scal = (C.c_double * max(1, len(pr.scal)))(*pr.scal)
+    st = scalar_state() if (norm or check) else None
+    N.check(N.lib().ek_vexpr(
+        int(length), code, len(pr.code), scal, len(pr.scal), N.ptrs(pr.ins),
+        len(pr.ins), N.ptrs(outs), len(outs), st.ptr if st else None,
+        work_ptr() if st else None, stream()), "ek_vexpr")
+    if st is None:
+        return None
+    h = st.read()
+    return float(h.val[1]), int(h.flag)
+
+
+def ev(expr, length=None, out=None):
+    """Evaluate one expression into a new (or given) device vector."""
+    if length is None:
+        length = _length(Expr.wrap(expr))
+    out = out if out is not None else empty(length)
+    evaluate([(expr, out)], length)
+    return out
+
+
+def _length(e):
+    if e.op == "vec":
+        return e.a.numel()
+    if e.op == "const":
+        return None
+    for c in (e.a, e.b):
+        if isinstance(c, Expr):
+            n = _length(c)
+            if n is not None:
+                return n
+    return None
+
+
+def copy(x):
+    out = empty(x.numel())
+    N.check(N.lib().ek_copy(C.c_void_p(out.data_ptr()), C.c_void_p(x.data_ptr()),
+                            x.numel() * 8, 3, stream()), "ek_copy")
+    return out
+
+
+def sqrt_eps():
+    return math.sqrt(float(np.finfo(np.float64).eps))

@@ -1,0 +1,115 @@
+// ek_common.cuh — shared device helpers for libexpkit_sm100.so.
+//
+// Deterministic reductions: every reducing kernel writes ONE partial per
+// block (slot b of `work`), then the last block to arrive (atomic ticket)
+// sums the partials in a fixed order (thread t takes b = t, t+256, ...;
+// then a fixed shuffle tree). The result is independent of block
+// scheduling, so repeated runs are bit-identical.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/expkit_sm100.h"
+
+namespace ek {
+
+constexpr int TPB = 256;               // threads per block, every kernel
+constexpr int NWARP = TPB / 32;
+constexpr double SQRT_EPS = 1.4901161193847656e-08;  // math.sqrt(2**-52), linalg.py:123
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+#define EK_LAUNCH_CHECK(where)                                                \
+    do {                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                  \
+        if (e_ != cudaSuccess) return ::ek::cuda_status(e_, where);           \
+    } while (0)
+
+__device__ __forceinline__ int flat_tid() {
+    return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+}
+__device__ __forceinline__ long flat_bid() {
+    return blockIdx.x + (long)gridDim.x * (blockIdx.y + (long)gridDim.y * blockIdx.z);
+}
+__device__ __forceinline__ long nblocks() {
+    return (long)gridDim.x * gridDim.y * gridDim.z;
+}
+
+// Sum NQ values over the block; the totals land in thread 0.
+template <int NQ>
+__device__ __forceinline__ void block_sum(double (&v)[NQ]) {
+    __shared__ double sh[NQ][NWARP];
+    const int t = flat_tid(), lane = t & 31, w = t >> 5;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
+    }
+    __syncthreads();  // protect sh from a previous use
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) sh[q][w] = v[q];
+    }
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            double x = lane < NWARP ? sh[q][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+            v[q] = x;
+        }
+    }
+}
+
+// Publish this block's NQ partials to work[b*NQ + q] and return true in the
+// last block to arrive (all threads of that block see true). The last block
+// resets the ticket for the next launch.
+template <int NQ>
+__device__ __forceinline__ bool publish_and_arrive(const double (&v)[NQ], double* work,
+                                                   uint32_t* ticket) {
+    __shared__ bool s_last;
+    const int t = flat_tid();
+    if (t == 0) {
+        const long b = flat_bid();
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) work[b * NQ + q] = v[q];
+        __threadfence();
+        const uint32_t got = atomicAdd(ticket, 1u);
+        s_last = (got == (uint32_t)(nblocks() - 1));
+        if (s_last) *ticket = 0u;
+    }
+    __syncthreads();
+    return s_last;
+}
+
+// In the last block: totals of the NQ partial channels, fixed order.
+// Result valid in thread 0.
+template <int NQ>
+__device__ __forceinline__ void gather_partials(const double* work, long nb, double (&tot)[NQ]) {
+    const int t = flat_tid();
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) tot[q] = 0.0;
+    for (long b = t; b < nb; b += TPB) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) tot[q] += __ldcg(work + b * NQ + q);
+    }
+    block_sum<NQ>(tot);
+}
+
+// x^3 with a double-double intermediate: the correctly rounded cube in all
+// but vanishingly rare cases, which is what NumPy's pow(x, 3) returns
+// (problems.py:94 `f**3`).
+__device__ __forceinline__ double cube_cr(double x) {
+    const double p = __dmul_rn(x, x);
+    const double pe = fma(x, x, -p);        // exact: x*x = p + pe
+    const double q = __dmul_rn(p, x);
+    const double qe = fma(p, x, -q);        // exact: p*x = q + qe
+    const double lo = fma(pe, x, qe);       // tiny correction
+    return __dadd_rn(q, lo);
+}
+
+}  // namespace ek

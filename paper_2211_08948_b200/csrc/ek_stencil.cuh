@@ -1,0 +1,681 @@
+// ek_stencil.cuh — fp64 2-D / 3-D stencil kernels of the phi-action path.
+//
+// One kernel template covers every fused pass that touches a stencil:
+//
+//   value  (EV_*)   : what is evaluated at each grid point
+//     EV_RHS     f(u)                                   problems.py rhs closures
+//     EV_FD      (f(u + eps*y) - fu) / eps              linalg.py:111-129
+//     EV_LIN     f(y)              (linear problems: exact Jacobian = f)
+//     EV_BURGJ   eta Lap y + d_x(u y) + d_y(u y)        Burgers analytic Jv
+//     EV_REMFD   (f(k) - fn) - (f(u + eps*(k-u)) - fn)/eps   integrators.py:99-109
+//     EV_REMLIN  (f(k) - fn) - f(k-u)
+//     EV_REMBURG (f(k) - fn) - J(u)(k-u)
+//   epilogue (EP_*)  : what is done with the value
+//     EP_STORE   out = value
+//     EP_LEJA    y' = value/gamma - shift*y ; p_i += d_i y' ; ||y'||^2 ;
+//                device-side freeze test (leja.py:172-184)
+//     EP_POWER   w = value ; ||w||^2 ; convergence test (spectrum.py:56-63)
+//     EP_ARN     w = dt*value + tail@uflip ; window dots (kiops.py:182-187)
+//     EP_REM     out = value ; non-finite flag (integrators.py:107-108)
+//
+// Geometry: axis 0 (i, slowest; the slab axis) is marched by each thread
+// over RPT consecutive rows/planes held in registers, so the vertical
+// neighbours are re-used instead of re-loaded; the contiguous axis is one
+// warp lane per column (coalesced 256-B row segments) with the +-1
+// neighbours exchanged by warp shuffles; in 3-D the middle axis comes from
+// the block's other warps through L1. Ghost rows follow the boundary
+// condition: reflect (np.pad 'reflect', Neumann), wrap (periodic), or the
+// halo buffers of a slab (multi-GPU).
+//
+// Arithmetic: every expression is written in NumPy's evaluation order and the
+// library is compiled with -fmad=false, so values match the reference's
+// elementwise results bit for bit (given identical inputs).
+#pragma once
+
+#include "ek_common.cuh"
+
+namespace ek {
+
+enum { EV_RHS = 0, EV_FD, EV_LIN, EV_BURGJ, EV_REMFD, EV_REMLIN, EV_REMBURG };
+enum { EP_STORE = 0, EP_LEJA, EP_POWER, EP_ARN, EP_REM };
+
+__host__ __device__ constexpr int ev_nch(int ev) {
+    return ev == EV_BURGJ ? 2 : ev == EV_REMFD ? 2 : ev == EV_REMLIN ? 2 : ev == EV_REMBURG ? 3 : 1;
+}
+__host__ __device__ constexpr int ep_nq(int ep) {
+    return ep == EP_LEJA ? 2 : ep == EP_POWER ? 2 : ep == EP_ARN ? 5 : ep == EP_REM ? 1 : 0;
+}
+
+struct Nb {
+    double c, xm, xp, ym, yp, zm, zp;  // centre, axis0 -/+, axis1 -/+, axis2 -/+
+};
+
+// ------------------------------------------------------------------ physics
+
+__device__ __forceinline__ double lap2(const Nb& s, double h2) {
+    return ((((s.xm + s.xp) + s.ym) + s.yp) - 4.0 * s.c) / h2;  // problems.py:28-29
+}
+__device__ __forceinline__ double lap3(const Nb& s, double h2) {
+    return ((((((s.xm + s.xp) + s.ym) + s.yp) + s.zm) + s.zp) - 6.0 * s.c) / h2;
+}
+// one-sided difference following the sign of +v.grad u (forward for v >= 0)
+__device__ __forceinline__ double upw_x(const Nb& s, double v, double h) {
+    return v >= 0.0 ? (s.xp - s.c) / h : (s.c - s.xm) / h;
+}
+__device__ __forceinline__ double upw_y(const Nb& s, double v, double h) {
+    return v >= 0.0 ? (s.yp - s.c) / h : (s.c - s.ym) / h;
+}
+__device__ __forceinline__ double upw_z(const Nb& s, double v, double h) {
+    return v >= 0.0 ? (s.zp - s.c) / h : (s.c - s.zm) / h;
+}
+
+// problems.py:69-83. prm: alpha, beta, gamma
+struct PAdr {
+    static constexpr int NC = 1, DIM = 2;
+    static constexpr bool LINEAR = false;
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+        const Nb& q = s[0];
+        const double lap = lap2(q, g.h2);
+        const double gx = (q.xp - q.xm) / g.two_h;
+        const double gy = (q.yp - q.ym) / g.two_h;
+        const double grad = gx + gy;
+        const double c = q.c;
+        o[0] = ((g.prm[0] * lap) + (g.prm[1] * grad)) + (((g.prm[2] * c) * (1.0 - c)) * (c - 0.5));
+    }
+};
+
+// problems.py:86-97 (and the periodic BASELINE variant). prm: alpha
+struct PAllenCahn {
+    static constexpr int NC = 1, DIM = 2;
+    static constexpr bool LINEAR = false;
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+        o[0] = ((g.prm[0] * lap2(s[0], g.h2)) + s[0].c) - cube_cr(s[0].c);
+    }
+};
+
+// problems.py:100-124. prm: alpha. STD selects form="standard" (u^2 v).
+template <bool STD>
+struct PBruss {
+    static constexpr int NC = 2, DIM = 2;
+    static constexpr bool LINEAR = false;
+    __device__ static void f(const Nb (&s)[2], double (&o)[2], const ek_grid& g) {
+        const double u = s[0].c, v = s[1].c;
+        const double uu_v = (u * u) * v;
+        const double react = STD ? uu_v : u * (v * v);
+        o[0] = (((g.prm[0] * lap2(s[0], g.h2)) + react) - (4.0 * u)) + 1.0;
+        o[1] = ((g.prm[0] * lap2(s[1], g.h2)) - uu_v) + (3.0 * u);
+    }
+};
+
+// problems.py:127-145. prm: alpha, a, a+b
+struct PGrayScott {
+    static constexpr int NC = 2, DIM = 2;
+    static constexpr bool LINEAR = false;
+    __device__ static void f(const Nb (&s)[2], double (&o)[2], const ek_grid& g) {
+        const double u = s[0].c, v = s[1].c;
+        const double uvv = u * (v * v);
+        o[0] = ((g.prm[0] * lap2(s[0], g.h2)) - uvv) + (g.prm[1] * (1.0 - u));
+        o[1] = ((g.prm[0] * lap2(s[1], g.h2)) + uvv) - (g.prm[2] * v);
+    }
+};
+
+// BASELINE config 1. prm: D, vx, vy. Linear: J = f.
+struct PAdvDiff2 {
+    static constexpr int NC = 1, DIM = 2;
+    static constexpr bool LINEAR = true;
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+        const Nb& q = s[0];
+        o[0] = ((g.prm[0] * lap2(q, g.h2)) + (g.prm[1] * upw_x(q, g.prm[1], g.h)))
+               + (g.prm[2] * upw_y(q, g.prm[2], g.h));
+    }
+};
+
+// BASELINE config 3. prm: eta.
+struct PBurgers {
+    static constexpr int NC = 1, DIM = 2;
+    static constexpr bool LINEAR = false;
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+        const Nb& q = s[0];
+        const double gx = ((q.xp * q.xp) - (q.xm * q.xm)) / g.two_h;
+        const double gy = ((q.yp * q.yp) - (q.ym * q.ym)) / g.two_h;
+        o[0] = ((g.prm[0] * lap2(q, g.h2)) + (0.5 * gx)) + (0.5 * gy);
+    }
+    // J(u) v = eta Lap v + d_x(u v) + d_y(u v)
+    __device__ static double jac(const Nb& u, const Nb& v, const ek_grid& g) {
+        const double gx = ((u.xp * v.xp) - (u.xm * v.xm)) / g.two_h;
+        const double gy = ((u.yp * v.yp) - (u.ym * v.ym)) / g.two_h;
+        return ((g.prm[0] * lap2(v, g.h2)) + gx) + gy;
+    }
+};
+
+// BASELINE config 5. prm: D, vx, vy, vz. Linear.
+struct PAdvDiff3 {
+    static constexpr int NC = 1, DIM = 3;
+    static constexpr bool LINEAR = true;
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+        const Nb& q = s[0];
+        o[0] = (((g.prm[0] * lap3(q, g.h2)) + (g.prm[1] * upw_x(q, g.prm[1], g.h)))
+                + (g.prm[2] * upw_y(q, g.prm[2], g.h)))
+               + (g.prm[3] * upw_z(q, g.prm[3], g.h));
+    }
+};
+
+// ------------------------------------------------------------- launch args
+
+struct KArgs {
+    ek_grid g;
+    long npts;            // points per component (local)
+    long n_aug;           // length of the tail (KIOPS p), 0 otherwise
+    // raw fields, component-major
+    const double* u;
+    const double* y;
+    const double* k;
+    const double* fu;
+    // slab halos: [2 sides][ncomp][row length]
+    const double* hu;
+    const double* hy;
+    const double* hk;
+    double* out;          // store target / next iterate
+    double* p[8];         // Leja accumulators
+    int nk;
+    int mi;               // column of the coefficient table
+    int m;                // iteration index
+    int jj;               // Arnoldi: index of the vector being built
+    const double* coef;   // Leja table: row 0 shift, rows 1..k d_i (32 wide)
+    double gamma;
+    double eps;           // host-provided FD increment (EP_STORE / EP_REM)
+    double dt;            // Arnoldi: operator scale (A.scaled(dt))
+    void* st;             // state block (type depends on the epilogue)
+    double* work;         // block partials
+    // Arnoldi
+    const double* win[4]; // window rows V[lo..jj-1] (n+p long), oldest first
+    int nwin;
+    const double* aug[5]; // nonzero augmentation vectors (u_flip rows / nu)
+    int aug_tail[5];      // tail index each of them multiplies
+    int naug;
+    double aug_scale;     // nu (power of two)
+    double* H;
+    int ldh;
+};
+
+// ----------------------------------------------------------------- geometry
+
+__device__ __forceinline__ long wrap_idx(long i, long n, int bc) {
+    if (i >= 0 && i < n) return i;
+    if (bc == EK_BC_PERIODIC) return i < 0 ? i + n : i - n;
+    if (n == 1) return 0;
+    return i < 0 ? 1 : n - 2;  // np.pad 'reflect': mirror without repeating the edge
+}
+
+// Base of row (2-D) / plane (3-D) `i` of component c of a field, i in [-1, rows].
+__device__ __forceinline__ const double* slab_row(const KArgs& a, const double* base,
+                                                  const double* halo, int c, long i,
+                                                  long rowlen) {
+    const long rows = a.g.rows;
+    if (i >= 0 && i < rows) return base + c * a.npts + i * rowlen;
+    if (a.g.slab) return halo + ((i < 0 ? 0 : 1) * (long)a.g.ncomp + c) * rowlen;
+    return base + c * a.npts + wrap_idx(i, rows, a.g.bc) * rowlen;
+}
+
+// Scalars a kernel reads from its state block before the sweep.
+struct Ctl {
+    double eps;
+    double ydiv;          // power iteration: v = w / ||w||
+    bool has_div;
+    uint32_t active;
+    double shift;
+    double d[8];
+    bool y_zero;          // FD closure shortcut: J 0 = 0 (integrators.py:89-90)
+    double augc[5];       // Arnoldi: tail[aug_tail[t]] * nu (exact: nu = 2^-e)
+};
+
+// Gather the channel values of one grid point (element pointer offsets are
+// per field because a ghost row may live in a halo buffer).
+template <int EV, int NCH>
+__device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const double* py,
+                                      const double* pk, long e, double (&ch)[NCH]) {
+    if constexpr (EV == EV_RHS) {
+        ch[0] = __ldg(pu + e);
+    } else if constexpr (EV == EV_FD) {
+        double yv = __ldg(py + e);
+        if (ctl.has_div) yv = yv / ctl.ydiv;
+        ch[0] = __ldg(pu + e) + ctl.eps * yv;  // u + eps*v   (linalg.py:126)
+    } else if constexpr (EV == EV_LIN) {
+        double yv = __ldg(py + e);
+        if (ctl.has_div) yv = yv / ctl.ydiv;
+        ch[0] = yv;
+    } else if constexpr (EV == EV_BURGJ) {
+        double yv = __ldg(py + e);
+        if (ctl.has_div) yv = yv / ctl.ydiv;
+        ch[0] = __ldg(pu + e);
+        ch[1] = yv;
+    } else if constexpr (EV == EV_REMFD) {
+        const double kv = __ldg(pk + e), uv = __ldg(pu + e);
+        const double dk = kv - uv;               // dk = k - u_n (integrators.py:103)
+        ch[0] = kv;
+        ch[1] = uv + ctl.eps * dk;
+    } else if constexpr (EV == EV_REMLIN) {
+        const double kv = __ldg(pk + e), uv = __ldg(pu + e);
+        ch[0] = kv;
+        ch[1] = kv - uv;
+    } else {  // EV_REMBURG
+        const double kv = __ldg(pk + e), uv = __ldg(pu + e);
+        ch[0] = kv;
+        ch[1] = uv;
+        ch[2] = kv - uv;
+    }
+}
+
+// Value at the centre from the channel neighbourhoods.
+template <class P, int EV, int NCH>
+__device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
+                                         const Nb (&nb)[P::NC][NCH], long off,
+                                         double (&val)[P::NC]) {
+    constexpr int NC = P::NC;
+    if constexpr (EV == EV_RHS || EV == EV_LIN) {
+        Nb s[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) s[c] = nb[c][0];
+        P::f(s, val, a.g);
+    } else if constexpr (EV == EV_FD) {
+        Nb s[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) s[c] = nb[c][0];
+        double fw[NC];
+        P::f(s, fw, a.g);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const double fuc = __ldg(a.fu + c * a.npts + off);
+            val[c] = ctl.y_zero ? 0.0 : (fw[c] - fuc) / ctl.eps;  // linalg.py:126
+        }
+    } else if constexpr (EV == EV_BURGJ) {
+        if constexpr (NC == 1 && NCH == 2) {
+            val[0] = PBurgers::jac(nb[0][0], nb[0][1], a.g);
+        }
+    } else if constexpr (EV == EV_REMFD) {
+        Nb s0[NC], s1[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { s0[c] = nb[c][0]; s1[c] = nb[c][1]; }
+        double fk[NC], fw[NC];
+        P::f(s0, fk, a.g);
+        P::f(s1, fw, a.g);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const double fn = __ldg(a.fu + c * a.npts + off);
+            val[c] = (fk[c] - fn) - ((fw[c] - fn) / ctl.eps);  // integrators.py:106
+        }
+    } else if constexpr (EV == EV_REMLIN) {
+        Nb s0[NC], s1[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) { s0[c] = nb[c][0]; s1[c] = nb[c][1]; }
+        double fk[NC], jd[NC];
+        P::f(s0, fk, a.g);
+        P::f(s1, jd, a.g);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const double fn = __ldg(a.fu + c * a.npts + off);
+            val[c] = (fk[c] - fn) - jd[c];
+        }
+    } else {  // EV_REMBURG
+        if constexpr (NC == 1 && NCH == 3) {
+            Nb s0[1] = {nb[0][0]};
+            double fk[1];
+            P::f(s0, fk, a.g);
+            const double fn = __ldg(a.fu + off);
+            val[0] = (fk[0] - fn) - PBurgers::jac(nb[0][1], nb[0][2], a.g);
+        }
+    }
+}
+
+// Read the state scalars; false = the iteration has already terminated.
+template <int EV, int EP>
+__device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
+    ctl.eps = a.eps;
+    ctl.ydiv = 1.0;
+    ctl.has_div = false;
+    ctl.active = 0u;
+    ctl.shift = 0.0;
+    ctl.y_zero = false;
+    if constexpr (EP == EP_LEJA) {
+        const ek_leja_state* st = (const ek_leja_state*)a.st;
+        if (st->done) return false;
+        ctl.eps = st->eps;
+        ctl.active = st->active;
+        ctl.y_zero = (EV == EV_FD) && (st->ny == 0.0);
+        ctl.shift = a.coef[a.mi];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ctl.d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
+    } else if constexpr (EP == EP_POWER) {
+        const ek_power_state* st = (const ek_power_state*)a.st;
+        if (st->done || st->status) return false;
+        ctl.ydiv = st->nw;  // v = w / ||w|| of the previous iterate
+        ctl.has_div = true;
+        ctl.eps = (SQRT_EPS * (1.0 + st->nu)) / st->nv;
+    } else if constexpr (EP == EP_ARN) {
+        const ek_arnoldi_state* st = (const ek_arnoldi_state*)a.st;
+        if (st->happy || st->status) return false;
+        ctl.eps = (SQRT_EPS * (1.0 + st->nu)) / st->nvn;
+        ctl.y_zero = (EV == EV_FD) && (st->nvn == 0.0);
+        const long n = (long)a.g.ncomp * a.npts;
+#pragma unroll
+        for (int t = 0; t < 5; ++t)
+            ctl.augc[t] = t < a.naug ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
+    }
+    return true;
+}
+
+// Per-point epilogue; acc[] collects this thread's partial reductions.
+template <int EV, int EP, int NC>
+__device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long off,
+                                         const double (&val)[NC], double* acc) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const long e = c * a.npts + off;
+        const double v = val[c];
+        if constexpr (EP == EP_STORE) {
+            a.out[e] = v;
+        } else if constexpr (EP == EP_LEJA) {
+            // y = J.apply(y)/gamma - (c/gamma + xi[m-1]) * y      leja.py:172
+            const double yn = (v / a.gamma) - (ctl.shift * __ldg(a.y + e));
+            a.out[e] = yn;
+            acc[0] += yn * yn;
+            if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q < a.nk && ((ctl.active >> q) & 1u)) {
+                    double* pq = a.p[q];
+                    pq[e] = pq[e] + (ctl.d[q] * yn);  // ps[i] + dds[i][m]*y  leja.py:179
+                }
+            }
+        } else if constexpr (EP == EP_POWER) {
+            a.out[e] = v;
+            acc[0] += v * v;
+            if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
+        } else if constexpr (EP == EP_ARN) {
+            // V[j,:n] = op.apply(V[j-1,:n]) + V[j-1,n:] @ u_flip    kiops.py:182
+            double augv = 0.0;
+#pragma unroll
+            for (int t = 0; t < 5; ++t)
+                if (t < a.naug) augv = augv + (ctl.augc[t] * __ldg(a.aug[t] + e));
+            const double w = (a.dt * v) + augv;
+            a.out[e] = w;
+            for (int q = 0; q < a.nwin; ++q) acc[q] += __ldg(a.win[q] + e) * w;
+            if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
+        } else {  // EP_REM
+            a.out[e] = v;
+            acc[0] += isfinite(v) ? 0.0 : 1.0;
+        }
+    }
+}
+
+// Last-block bookkeeping of one fused pass.
+template <int EV, int EP>
+__device__ void finalize(const KArgs& a, const double* tot);
+
+// ------------------------------------------------------------ 2-D kernel
+
+template <class P, int EV, int EP, int RPT>
+__global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
+    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    Ctl ctl;
+    if (!load_ctl<EV, EP>(a, ctl)) return;
+    const int lane = threadIdx.x, ty = threadIdx.y;
+    const long cols = a.g.n, rows = a.g.rows;
+    const long j = (long)blockIdx.x * 32 + lane;
+    const long i0 = ((long)blockIdx.y * 8 + ty) * RPT;
+    const long jc = j < cols ? j : cols - 1;
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+
+    if (i0 < rows) {  // warp-uniform
+        const long jw = wrap_idx(jc - 1, cols, a.g.bc);
+        const long je = wrap_idx(jc + 1, cols, a.g.bc);
+        const bool needW = lane == 0;
+        const bool needE = lane == 31 || jc == cols - 1;
+        double cv[RPT + 2][NC][NCH];
+        double cw[RPT][NC][NCH], ce[RPT][NC][NCH];
+#pragma unroll
+        for (int r = 0; r < RPT + 2; ++r) {
+            long i = i0 - 1 + r;
+            if (i > rows) i = rows;  // beyond the ghost row: clamp (unused)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const double* pu = slab_row(a, a.u, a.hu, c, i, cols);
+                const double* py = slab_row(a, a.y, a.hy, c, i, cols);
+                const double* pk = slab_row(a, a.k, a.hk, c, i, cols);
+                fetch<EV, NCH>(ctl, pu, py, pk, jc, cv[r][c]);
+                if (r >= 1 && r <= RPT) {
+                    if (needW) fetch<EV, NCH>(ctl, pu, py, pk, jw, cw[r - 1][c]);
+                    if (needE) fetch<EV, NCH>(ctl, pu, py, pk, je, ce[r - 1][c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 1; r <= RPT; ++r) {
+            const long i = i0 + r - 1;
+            Nb nb[NC][NCH];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) {
+                    const double cc = cv[r][c][h];
+                    double w = __shfl_up_sync(0xffffffffu, cc, 1);
+                    double e = __shfl_down_sync(0xffffffffu, cc, 1);
+                    if (needW) w = cw[r - 1][c][h];
+                    if (needE) e = ce[r - 1][c][h];
+                    nb[c][h].c = cc;
+                    nb[c][h].xm = cv[r - 1][c][h];
+                    nb[c][h].xp = cv[r + 1][c][h];
+                    nb[c][h].ym = w;
+                    nb[c][h].yp = e;
+                    nb[c][h].zm = 0.0;
+                    nb[c][h].zp = 0.0;
+                }
+            }
+            if (i < rows && j < cols) {
+                const long off = i * cols + j;
+                double val[NC];
+                evaluate<P, EV, NCH>(a, ctl, nb, off, val);
+                epilogue<EV, EP, NC>(a, ctl, off, val, acc);
+            }
+        }
+    }
+    if constexpr (ep_nq(EP) > 0) {
+        block_sum<NQ>(acc);
+        uint32_t* ticket = nullptr;
+        if constexpr (EP == EP_LEJA) ticket = &((ek_leja_state*)a.st)->ticket;
+        else if constexpr (EP == EP_POWER) ticket = &((ek_power_state*)a.st)->ticket;
+        else if constexpr (EP == EP_ARN) ticket = &((ek_arnoldi_state*)a.st)->ticket;
+        else ticket = &((ek_scalar_state*)a.st)->ticket;
+        if (publish_and_arrive<NQ>(acc, a.work, ticket)) {
+            double tot[NQ];
+            gather_partials<NQ>(a.work, nblocks(), tot);
+            if (flat_tid() == 0) finalize<EV, EP>(a, tot);
+        }
+    }
+}
+
+// ------------------------------------------------------------ 3-D kernel
+// lanes along k (axis 2), threadIdx.y along j (axis 1), RPT planes of i.
+
+template <class P, int EV, int EP, int RPT>
+__global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
+    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    Ctl ctl;
+    if (!load_ctl<EV, EP>(a, ctl)) return;
+    const int lane = threadIdx.x, ty = threadIdx.y;
+    const long n = a.g.n, rows = a.g.rows, plane = n * n;
+    const long kx = (long)blockIdx.x * 32 + lane;
+    const long jy = (long)blockIdx.y * 8 + ty;
+    const long i0 = (long)blockIdx.z * RPT;
+    const long kc = kx < n ? kx : n - 1;
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+
+    if (i0 < rows && jy < n) {  // warp-uniform
+        const long kw = wrap_idx(kc - 1, n, a.g.bc), ke = wrap_idx(kc + 1, n, a.g.bc);
+        const long jm = wrap_idx(jy - 1, n, a.g.bc), jp = wrap_idx(jy + 1, n, a.g.bc);
+        const bool needW = lane == 0;
+        const bool needE = lane == 31 || kc == n - 1;
+        double cv[RPT + 2][NC][NCH];
+        double cjm[RPT][NC][NCH], cjp[RPT][NC][NCH];
+        double cw[RPT][NC][NCH], ce[RPT][NC][NCH];
+#pragma unroll
+        for (int r = 0; r < RPT + 2; ++r) {
+            long i = i0 - 1 + r;
+            if (i > rows) i = rows;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const double* pu = slab_row(a, a.u, a.hu, c, i, plane);
+                const double* py = slab_row(a, a.y, a.hy, c, i, plane);
+                const double* pk = slab_row(a, a.k, a.hk, c, i, plane);
+                fetch<EV, NCH>(ctl, pu, py, pk, jy * n + kc, cv[r][c]);
+                if (r >= 1 && r <= RPT) {
+                    fetch<EV, NCH>(ctl, pu, py, pk, jm * n + kc, cjm[r - 1][c]);
+                    fetch<EV, NCH>(ctl, pu, py, pk, jp * n + kc, cjp[r - 1][c]);
+                    if (needW) fetch<EV, NCH>(ctl, pu, py, pk, jy * n + kw, cw[r - 1][c]);
+                    if (needE) fetch<EV, NCH>(ctl, pu, py, pk, jy * n + ke, ce[r - 1][c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 1; r <= RPT; ++r) {
+            const long i = i0 + r - 1;
+            Nb nb[NC][NCH];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) {
+                    const double cc = cv[r][c][h];
+                    double w = __shfl_up_sync(0xffffffffu, cc, 1);
+                    double e = __shfl_down_sync(0xffffffffu, cc, 1);
+                    if (needW) w = cw[r - 1][c][h];
+                    if (needE) e = ce[r - 1][c][h];
+                    nb[c][h].c = cc;
+                    nb[c][h].xm = cv[r - 1][c][h];
+                    nb[c][h].xp = cv[r + 1][c][h];
+                    nb[c][h].ym = cjm[r - 1][c][h];
+                    nb[c][h].yp = cjp[r - 1][c][h];
+                    nb[c][h].zm = w;
+                    nb[c][h].zp = e;
+                }
+            }
+            if (i < rows && kx < n) {
+                const long off = i * plane + jy * n + kx;
+                double val[NC];
+                evaluate<P, EV, NCH>(a, ctl, nb, off, val);
+                epilogue<EV, EP, NC>(a, ctl, off, val, acc);
+            }
+        }
+    }
+    if constexpr (ep_nq(EP) > 0) {
+        block_sum<NQ>(acc);
+        uint32_t* ticket = nullptr;
+        if constexpr (EP == EP_LEJA) ticket = &((ek_leja_state*)a.st)->ticket;
+        else if constexpr (EP == EP_POWER) ticket = &((ek_power_state*)a.st)->ticket;
+        else if constexpr (EP == EP_ARN) ticket = &((ek_arnoldi_state*)a.st)->ticket;
+        else ticket = &((ek_scalar_state*)a.st)->ticket;
+        if (publish_and_arrive<NQ>(acc, a.work, ticket)) {
+            double tot[NQ];
+            gather_partials<NQ>(a.work, nblocks(), tot);
+            if (flat_tid() == 0) finalize<EV, EP>(a, tot);
+        }
+    }
+}
+
+// --------------------------------------------------------------- finalize
+
+template <int EV, int EP>
+__device__ void finalize(const KArgs& a, const double* tot) {
+    if constexpr (EP == EP_LEJA) {
+        ek_leja_state* st = (ek_leja_state*)a.st;
+        const int m = a.m;
+        const double ny = sqrt(tot[0]);  // np.linalg.norm(y)   leja.py:173
+        if (EV == EV_FD && st->ny != 0.0) st->fd_evals += 1;
+        if (EV == EV_FD && tot[1] > 0.0) {
+            st->status = EK_ST_JV_NONFINITE;  // linalg.py:127-128
+            st->done = 1;
+            st->iters = m;
+            return;
+        }
+        if (!isfinite(ny)) {
+            st->status = EK_ST_NORM_NONFINITE;  // leja.py:174-175
+            st->done = 1;
+            st->iters = m;
+            return;
+        }
+        uint32_t act = st->active;
+        for (int q = 0; q < a.nk; ++q) {
+            if ((act >> q) & 1u) {
+                const double dq = a.coef[(1 + q) * 32 + a.mi];
+                if (fabs(dq) * ny < st->tol) {  // leja.py:180
+                    act &= ~(1u << q);
+                    st->freeze[q] = m;
+                }
+            }
+        }
+        st->active = act;
+        st->ny = ny;
+        st->m = m;
+        st->eps = (SQRT_EPS * (1.0 + st->nu)) / ny;  // linalg.py:123
+        if (act == 0u) {
+            st->done = 1;
+            st->iters = m;
+        }
+    } else if constexpr (EP == EP_POWER) {
+        ek_power_state* st = (ek_power_state*)a.st;
+        const double nw = sqrt(tot[0]);  // spectrum.py:58
+        if (EV == EV_FD) st->fd_evals += 1;
+        if (EV == EV_FD && tot[1] > 0.0) {
+            st->status = EK_ST_JV_NONFINITE;
+            st->done = 1;
+            return;
+        }
+        st->it += 1;
+        if (nw == 0.0) {  // spectrum.py:59-60
+            st->lam = 0.0;
+            st->converged = 1;
+            st->done = 1;
+        } else if (fabs(nw - st->lam) <= st->tol_pi * nw) {  // spectrum.py:63
+            st->lam = nw;
+            st->converged = 1;
+            st->done = 1;
+        } else {
+            st->lam = nw;
+            if (st->it >= st->max_it) st->done = 1;
+        }
+        st->nw = nw;
+    } else if constexpr (EP == EP_ARN) {
+        ek_arnoldi_state* st = (ek_arnoldi_state*)a.st;
+        if (EV == EV_FD && st->nvn != 0.0) st->fd_evals += 1;
+        if (EV == EV_FD && tot[4] > 0.0) {
+            st->status = EK_ST_JV_NONFINITE;
+            return;
+        }
+        // tail of V[j]: shift of the previous tail, last entry 0 (kiops.py:183-184)
+        const long n = a.g.ncomp * a.npts;
+        const int p = (int)a.n_aug;
+        const double* prev = a.win[a.nwin - 1];
+        double* cur = a.out;
+        for (int t = 0; t + 1 < p; ++t) cur[n + t] = prev[n + t + 1];
+        if (p > 0) cur[n + p - 1] = 0.0;
+        const int jj = a.jj;
+        const int lo = jj - a.nwin;
+        for (int q = 0; q < a.nwin; ++q) {
+            double tail = 0.0;
+            for (int t = 0; t < p; ++t) tail += a.win[q][n + t] * cur[n + t];
+            a.H[(long)(lo + q) * a.ldh + (jj - 1)] = tot[q] + tail;  // kiops.py:187
+        }
+        a.H[(long)jj * a.ldh + (jj - 1)] = 0.0;
+    } else if constexpr (EP == EP_REM) {
+        ek_scalar_state* st = (ek_scalar_state*)a.st;
+        if (tot[0] > 0.0) {
+            st->flag |= 2;
+            st->status = EK_ST_REM_NONFINITE;
+        }
+    }
+}
+
+}  // namespace ek

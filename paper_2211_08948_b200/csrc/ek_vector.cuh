@@ -1,0 +1,478 @@
+// ek_vector.cuh — non-stencil fp64 vector kernels (grid-stride, fixed grid
+// per length so reductions are deterministic).
+#pragma once
+
+#include "ek_common.cuh"
+
+namespace ek {
+
+constexpr int VGRID_MAX = 148 * 16;  // 16 resident 256-thread blocks per SM
+
+__host__ __forceinline__ int vgrid(int64_t len) {
+    int64_t b = (len + TPB - 1) / TPB;
+    if (b < 1) b = 1;
+    return (int)(b < VGRID_MAX ? b : VGRID_MAX);
+}
+
+// ---------------------------------------------------------------- norms
+// ||x||^2 (+ flags: bit0 any nonzero, bit1 any non-finite) -> st->val[slot]
+// = ssq, st->val[slot+1] = sqrt(ssq). `div` (nullable) scales on read.
+__global__ void __launch_bounds__(TPB) k_norm2(int64_t len, const double* __restrict__ x,
+                                               const double* div, ek_scalar_state* st,
+                                               int slot, double* work) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    const double d = div ? *div : 1.0;
+    const bool has_div = div != nullptr;
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * TPB) {
+        double v = __ldg(x + e);
+        if (has_div) v = v / d;
+        acc[0] += v * v;
+        acc[1] += (v != 0.0) ? 1.0 : 0.0;
+        acc[2] += isfinite(v) ? 0.0 : 1.0;
+    }
+    block_sum<3>(acc);
+    if (publish_and_arrive<3>(acc, work, &st->ticket)) {
+        double tot[3];
+        gather_partials<3>(work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            st->val[slot] = tot[0];
+            st->val[slot + 1] = sqrt(tot[0]);
+            st->flag |= (tot[1] > 0.0 ? 1 : 0) | (tot[2] > 0.0 ? 2 : 0);
+        }
+    }
+}
+
+// sum |x_e| -> st->val[slot]  (kiops.py:146 L1 norms of the augmentation)
+__global__ void __launch_bounds__(TPB) k_l1(int64_t len, const double* __restrict__ x,
+                                            ek_scalar_state* st, int slot, double* work) {
+    double acc[1] = {0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * TPB)
+        acc[0] += fabs(__ldg(x + e));
+    block_sum<1>(acc);
+    if (publish_and_arrive<1>(acc, work, &st->ticket)) {
+        double tot[1];
+        gather_partials<1>(work, gridDim.x, tot);
+        if (threadIdx.x == 0) st->val[slot] = tot[0];
+    }
+}
+
+// ------------------------------------------------------------------ Leja
+struct LejaVArgs {
+    int64_t len;
+    const double* b;      // begin: start vector; update: Jacobian action
+    const double* y;      // update: previous iterate
+    double* ynext;
+    double* p[8];
+    int nk;
+    const double* coef;
+    int mi;
+    int m;
+    double gamma;
+    ek_leja_state* st;
+    double* work;
+};
+
+// m = 0 of the Newton-Leja sum (leja.py:159-165).
+__global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
+    double acc[1] = {0.0};
+    double d[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
+         e += (int64_t)gridDim.x * TPB) {
+        const double y = __ldg(a.b + e);
+        acc[0] += y * y;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < a.nk) a.p[q][e] = d[q] * y;  // dds[i][0] * y
+    }
+    block_sum<1>(acc);
+    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
+        double tot[1];
+        gather_partials<1>(a.work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            ek_leja_state* st = a.st;
+            const double ny = sqrt(tot[0]);
+            uint32_t act = 0u;
+            for (int q = 0; q < a.nk; ++q) {
+                if (!(fabs(d[q]) * ny < st->tol)) act |= 1u << q;
+                st->freeze[q] = 0;
+            }
+            st->active = act;
+            st->ny = ny;
+            st->m = 0;
+            st->status = EK_ST_OK;
+            st->eps = (SQRT_EPS * (1.0 + st->nu)) / ny;
+            st->done = act == 0u ? 1 : 0;
+            st->iters = 0;
+        }
+    }
+}
+
+// One recurrence step for a Jacobian action computed elsewhere
+// (dense / callable / 1-D operators).
+__global__ void __launch_bounds__(TPB) k_leja_update(const LejaVArgs a) {
+    const ek_leja_state* cst = a.st;
+    if (cst->done) return;
+    const double shift = a.coef[a.mi];
+    const uint32_t act = cst->active;
+    double d[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
+    double acc[1] = {0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
+         e += (int64_t)gridDim.x * TPB) {
+        const double yn = (__ldg(a.b + e) / a.gamma) - (shift * __ldg(a.y + e));
+        a.ynext[e] = yn;
+        acc[0] += yn * yn;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < a.nk && ((act >> q) & 1u)) a.p[q][e] = a.p[q][e] + (d[q] * yn);
+    }
+    block_sum<1>(acc);
+    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
+        double tot[1];
+        gather_partials<1>(a.work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            ek_leja_state* st = a.st;
+            const int m = a.m;
+            const double ny = sqrt(tot[0]);
+            if (!isfinite(ny)) {
+                st->status = EK_ST_NORM_NONFINITE;
+                st->done = 1;
+                st->iters = m;
+                return;
+            }
+            uint32_t ac = st->active;
+            for (int q = 0; q < a.nk; ++q) {
+                if (((ac >> q) & 1u) && fabs(d[q]) * ny < st->tol) {
+                    ac &= ~(1u << q);
+                    st->freeze[q] = m;
+                }
+            }
+            st->active = ac;
+            st->ny = ny;
+            st->m = m;
+            st->eps = (SQRT_EPS * (1.0 + st->nu)) / ny;
+            if (ac == 0u) {
+                st->done = 1;
+                st->iters = m;
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------- KIOPS
+struct ArnVArgs {
+    int64_t n;            // operator dimension (the n-part)
+    int p;                // tail length
+    const double* jv;     // generic augment: op.apply(V[j-1,:n]) (already scaled)
+    const double* win[4]; // window rows V[lo..jj-1]
+    int nwin;
+    const double* aug[5];
+    int aug_tail[5];
+    int naug;
+    double aug_scale;
+    double* w;            // V[jj]
+    double* H;
+    int ldh;
+    int jj;
+    double tail0[5];      // init: tail values of V[0]
+    const double* src;    // init: V[0][:n] source
+    ek_arnoldi_state* st;
+    double* work;
+};
+
+// V[0] = [w_l ; tail], beta = ||V[0]||  (kiops.py:168-176)
+__global__ void __launch_bounds__(TPB) k_arn_init(const ArnVArgs a) {
+    double acc[1] = {0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.n;
+         e += (int64_t)gridDim.x * TPB) {
+        const double v = __ldg(a.src + e);
+        a.w[e] = v;
+        acc[0] += v * v;
+    }
+    block_sum<1>(acc);
+    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
+        double tot[1];
+        gather_partials<1>(a.work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            double ssq = tot[0];
+            for (int t = 0; t < a.p; ++t) {
+                a.w[a.n + t] = a.tail0[t];
+                ssq += a.tail0[t] * a.tail0[t];
+            }
+            const double beta = sqrt(ssq);
+            a.st->nrm = beta;
+            a.st->beta = beta;
+            a.st->happy = 0;
+            a.st->status = EK_ST_OK;
+            a.st->j = 0;
+        }
+    }
+}
+
+// generic pass A: w[:n] = jv + tail@uflip, tail shift, window dots
+__global__ void __launch_bounds__(TPB) k_arn_augment(const ArnVArgs a) {
+    const ek_arnoldi_state* cst = a.st;
+    if (cst->happy || cst->status) return;
+    double augc[5];  // tail * nu, exact because nu is a power of two
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+        augc[t] = t < a.naug ? a.win[a.nwin - 1][a.n + a.aug_tail[t]] * a.aug_scale : 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.n;
+         e += (int64_t)gridDim.x * TPB) {
+        double augv = 0.0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t)
+            if (t < a.naug) augv = augv + (augc[t] * __ldg(a.aug[t] + e));
+        const double w = __ldg(a.jv + e) + augv;
+        a.w[e] = w;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q < a.nwin) acc[q] += __ldg(a.win[q] + e) * w;
+    }
+    block_sum<4>(acc);
+    if (publish_and_arrive<4>(acc, a.work, &a.st->ticket)) {
+        double tot[4];
+        gather_partials<4>(a.work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            const int64_t n = a.n;
+            const double* prev = a.win[a.nwin - 1];
+            for (int t = 0; t + 1 < a.p; ++t) a.w[n + t] = prev[n + t + 1];
+            if (a.p > 0) a.w[n + a.p - 1] = 0.0;
+            const int lo = a.jj - a.nwin;
+            for (int q = 0; q < a.nwin; ++q) {
+                double tl = 0.0;
+                for (int t = 0; t < a.p; ++t) tl += a.win[q][n + t] * a.w[n + t];
+                a.H[(long)(lo + q) * a.ldh + (a.jj - 1)] = tot[q] + tl;
+            }
+            a.H[(long)a.jj * a.ldh + (a.jj - 1)] = 0.0;
+        }
+    }
+}
+
+// pass B: V[j] -= V[lo:j].T @ H[lo:j, j-1]; nrm = ||V[j]||; happy test
+// (kiops.py:188-193). Runs over the full n+p row.
+__global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
+    const ek_arnoldi_state* cst = a.st;
+    if (cst->happy || cst->status) return;
+    const int lo = a.jj - a.nwin;
+    double h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) h[q] = q < a.nwin ? a.H[(long)(lo + q) * a.ldh + (a.jj - 1)] : 0.0;
+    const int64_t len = a.n + a.p;
+    double acc[1] = {0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * TPB) {
+        double t = __ldg(a.win[0] + e) * h[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q)
+            if (q < a.nwin) t = t + (__ldg(a.win[q] + e) * h[q]);
+        const double w = a.w[e] - t;
+        a.w[e] = w;
+        acc[0] += w * w;
+    }
+    block_sum<1>(acc);
+    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
+        double tot[1];
+        gather_partials<1>(a.work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            ek_arnoldi_state* st = a.st;
+            const double nrm = sqrt(tot[0]);
+            st->nrm = nrm;
+            if (nrm < st->tol) {  // happy breakdown, kiops.py:190-192
+                st->happy = 1;
+                st->j = a.jj;
+            } else {
+                a.H[(long)a.jj * a.ldh + (a.jj - 1)] = nrm;
+            }
+        }
+    }
+}
+
+// pass C: V[j] /= nrm; ||V[j,:n]|| for the next FD increment (kiops.py:194).
+__global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
+    const ek_arnoldi_state* cst = a.st;
+    if (cst->happy || cst->status) return;
+    const double nrm = cst->nrm;
+    const int64_t len = a.n + a.p;
+    double acc[1] = {0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * TPB) {
+        const double v = a.w[e] / nrm;
+        a.w[e] = v;
+        if (e < a.n) acc[0] += v * v;
+    }
+    block_sum<1>(acc);
+    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
+        double tot[1];
+        gather_partials<1>(a.work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            a.st->nvn = sqrt(tot[0]);
+            a.st->j = a.jj;
+        }
+    }
+}
+
+// out = sum_i coef[i] * V_i[:n]   (kiops.py:267, 270)
+constexpr int MAXB = 136;
+struct CombineArgs {
+    int64_t n;
+    int j;
+    double* out;
+    const double* rows[MAXB];
+    double coef[MAXB];
+};
+__global__ void __launch_bounds__(TPB) k_basis_combine(const CombineArgs a) {
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.n;
+         e += (int64_t)gridDim.x * TPB) {
+        double s = a.coef[0] * __ldg(a.rows[0] + e);
+        for (int i = 1; i < a.j; ++i) s = s + (a.coef[i] * __ldg(a.rows[i] + e));
+        a.out[e] = s;
+    }
+}
+
+// ------------------------------------------------------------- power init
+// ||v0|| -> st->nw (the divisor of the first iterate), FD: ||v0/||v0|| || -> nv
+__global__ void __launch_bounds__(TPB) k_power_norm(int64_t len, const double* __restrict__ x,
+                                                    int scaled, ek_power_state* st,
+                                                    double* work) {
+    if (scaled && (st->done || st->status)) return;
+    const double d = st->nw;
+    double acc[1] = {0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
+         e += (int64_t)gridDim.x * TPB) {
+        double v = __ldg(x + e);
+        if (scaled) v = v / d;
+        acc[0] += v * v;
+    }
+    block_sum<1>(acc);
+    if (publish_and_arrive<1>(acc, work, &st->ticket)) {
+        double tot[1];
+        gather_partials<1>(work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+            if (scaled) st->nv = sqrt(tot[0]);
+            else st->nw = sqrt(tot[0]);
+        }
+    }
+}
+
+// ----------------------------------------------------------------- vexpr
+// Elementwise stack program, NumPy order. Opcode word: op | (arg << 8).
+enum {
+    VX_LOAD = 1,   // push in[arg][e]
+    VX_CONST = 2,  // push scal[arg]
+    VX_ADD = 3, VX_SUB = 4, VX_MUL = 5, VX_DIV = 6, VX_NEG = 7,
+    VX_STORE = 8,  // out[arg][e] = top (keeps it)
+    VX_POP = 9,
+    VX_NORM = 10,  // acc[arg] += top*top
+    VX_CHECK = 11, // flags: bit0 nonzero, bit1 non-finite (of top)
+    VX_ACC = 12    // acc[arg] += top   (dot products)
+};
+constexpr int VX_MAXPROG = 48;
+struct VexprArgs {
+    int64_t len;
+    int nprog;
+    int32_t prog[VX_MAXPROG];
+    double scal[16];
+    const double* in[8];
+    double* out[4];
+    ek_scalar_state* st;
+    double* work;
+    int reduce;  // 1 if the program has NORM/CHECK ops
+};
+__global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // 0,1: norms ; 2: nonzero ; 3: non-finite
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
+         e += (int64_t)gridDim.x * TPB) {
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0;  // register stack
+        int sp = 0;
+#define VX_PUSH(v)                                  \
+    do {                                            \
+        const double v_ = (v);                      \
+        switch (sp) {                               \
+            case 0: s0 = v_; break;                 \
+            case 1: s1 = v_; break;                 \
+            case 2: s2 = v_; break;                 \
+            case 3: s3 = v_; break;                 \
+            case 4: s4 = v_; break;                 \
+            default: s5 = v_; break;                \
+        }                                           \
+        ++sp;                                       \
+    } while (0)
+#define VX_AT(i) ((i) == 0 ? s0 : (i) == 1 ? s1 : (i) == 2 ? s2 : (i) == 3 ? s3 : (i) == 4 ? s4 : s5)
+        for (int pc = 0; pc < a.nprog; ++pc) {
+            const int w = a.prog[pc];
+            const int op = w & 0xff, arg = w >> 8;
+            switch (op) {
+                case VX_LOAD: VX_PUSH(__ldg(a.in[arg] + e)); break;
+                case VX_CONST: VX_PUSH(a.scal[arg]); break;
+                case VX_NEG: {
+                    const double t = VX_AT(sp - 1);
+                    --sp;
+                    VX_PUSH(-t);
+                } break;
+                case VX_STORE: a.out[arg][e] = VX_AT(sp - 1); break;
+                case VX_POP: --sp; break;
+                case VX_NORM: {
+                    const double t = VX_AT(sp - 1);
+                    acc[arg] += t * t;
+                } break;
+                case VX_ACC: acc[arg] += VX_AT(sp - 1); break;
+                case VX_CHECK: {
+                    const double t = VX_AT(sp - 1);
+                    acc[2] += t != 0.0 ? 1.0 : 0.0;
+                    acc[3] += isfinite(t) ? 0.0 : 1.0;
+                } break;
+                default: {
+                    const double b = VX_AT(sp - 1);
+                    const double x = VX_AT(sp - 2);
+                    sp -= 2;
+                    double r;
+                    if (op == VX_ADD) r = x + b;
+                    else if (op == VX_SUB) r = x - b;
+                    else if (op == VX_MUL) r = x * b;
+                    else r = x / b;
+                    VX_PUSH(r);
+                } break;
+            }
+        }
+#undef VX_PUSH
+#undef VX_AT
+    }
+    if (a.reduce) {
+        block_sum<4>(acc);
+        if (publish_and_arrive<4>(acc, a.work, &a.st->ticket)) {
+            double tot[4];
+            gather_partials<4>(a.work, gridDim.x, tot);
+            if (threadIdx.x == 0) {
+                a.st->val[0] = tot[0];
+                a.st->val[1] = sqrt(tot[0]);
+                a.st->val[2] = tot[1];
+                a.st->val[3] = sqrt(tot[1]);
+                a.st->flag |= (tot[2] > 0.0 ? 1 : 0) | (tot[3] > 0.0 ? 2 : 0);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ dense GEMV
+// y = A x, one warp per row, fixed lane order (linalg.py:87-90).
+__global__ void __launch_bounds__(TPB) k_dense_gemv(int64_t n, const double* __restrict__ A,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = ((int64_t)blockIdx.x * TPB + threadIdx.x) >> 5;
+    if (row >= n) return;
+    double s = 0.0;
+    for (int64_t c = lane; c < n; c += 32) s += __ldg(A + row * n + c) * __ldg(x + c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) y[row] = s;
+}
+
+}  // namespace ek

@@ -1,0 +1,627 @@
+// expkit_sm100.cu — C ABI of libexpkit_sm100.so (see include/expkit_sm100.h).
+//
+// Host-side launchers: pick the kernel instance for (problem, value,
+// epilogue), size the grid, and loop over iterations on the stream without
+// host synchronisation (the iteration state lives in device memory).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <type_traits>
+
+#include "ek_common.cuh"
+#include "ek_stencil.cuh"
+#include "ek_vector.cuh"
+
+namespace ek {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+    set_error("%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+    return EK_ERR_CUDA;
+}
+
+// ------------------------------------------------------------- 1-D problem
+// problems.py:154-196: semilinear, Dirichlet, nonlocal trapezoid integral.
+// One block; thread 0 reproduces NumPy's pairwise summation order
+// (loops_utils.h pairwise_sum) for np.sum(u).
+
+struct SemiArgs {
+    int64_t n;         // interior points; the vector has n+1 entries
+    double h, h2, h24; // h, h**2, h/24.0
+    int mode;          // 0: f(u)  1: (f(u+eps y)-fu)/eps  2: J(t_n) y
+    const double* u;
+    const double* y;
+    const double* fu;
+    double eps;
+    double* out;
+    ek_scalar_state* st;  // optional: non-finite flag (mode 1)
+};
+
+__device__ __forceinline__ double semi_in(const SemiArgs& a, int64_t i) {
+    if (a.mode == 0) return a.u[i];
+    if (a.mode == 1) return a.u[i] + a.eps * a.y[i];
+    return a.y[i];
+}
+
+__device__ double semi_pairwise(const SemiArgs& a, int64_t lo, int64_t n) {
+    if (n < 8) {
+        double r = -0.0;
+        for (int64_t i = 0; i < n; ++i) r += semi_in(a, lo + i);
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int q = 0; q < 8; ++q) r[q] = semi_in(a, lo + q);
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int q = 0; q < 8; ++q) r[q] += semi_in(a, lo + i + q);
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += semi_in(a, lo + i);
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return semi_pairwise(a, lo, n2) + semi_pairwise(a, lo + n2, n - n2);
+}
+
+__device__ __forceinline__ double semi_forcing(double x, double t) {
+    return exp(t) * (((x * (1.0 - x)) + 2.0) - (1.0 / 6.0));  // problems.py:148-151
+}
+
+__global__ void __launch_bounds__(TPB) k_semilinear(const SemiArgs a) {
+    __shared__ double s_q;
+    __shared__ int s_bad;
+    const int64_t n = a.n;
+    if (threadIdx.x == 0) {
+        s_bad = 0;
+        const double S = semi_pairwise(a, 0, n);
+        const double w0 = semi_in(a, 0), w1 = n > 1 ? semi_in(a, 1) : 0.0;
+        const double wl = semi_in(a, n - 1), wl2 = n > 1 ? semi_in(a, n - 2) : 0.0;
+        const double corr = a.h24 * ((((4.0 * w0) - w1) + (4.0 * wl)) - wl2);  // problems.py:167
+        s_q = (a.h * S) + corr;
+    }
+    __syncthreads();
+    const double q = s_q;
+    const double t = semi_in(a, n);  // time component
+    const double tn = a.u[n];         // linearisation time (mode 2)
+    int bad = 0;
+    for (int64_t i = threadIdx.x; i <= n; i += TPB) {
+        double r;
+        if (i == n) {
+            r = a.mode == 0 ? 1.0 : a.mode == 1 ? (1.0 - a.fu[n]) / a.eps : 0.0;
+        } else {
+            const double wm = i > 0 ? semi_in(a, i - 1) : 0.0;
+            const double wp = i + 1 < n ? semi_in(a, i + 1) : 0.0;
+            const double wi = semi_in(a, i);
+            const double d2 = ((wm - (2.0 * wi)) + wp) / a.h2;  // problems.py:172-173
+            const double x = a.h * (double)(i + 1);
+            if (a.mode == 2) {
+                r = (d2 + q) + (semi_forcing(x, tn) * t);  // problems.py:186
+            } else {
+                r = (d2 + q) + semi_forcing(x, t);  // problems.py:174
+                if (a.mode == 1) r = (r - a.fu[i]) / a.eps;
+            }
+        }
+        a.out[i] = r;
+        bad |= isfinite(r) ? 0 : 1;
+    }
+    if (a.st && bad) atomicOr(&s_bad, 1);
+    __syncthreads();
+    if (a.st && threadIdx.x == 0 && s_bad) a.st->flag |= 2;
+}
+
+// --------------------------------------------------------------- dispatch
+
+static int64_t grid_points(const ek_grid* g) {
+    if (g->dim == 1) return g->n;
+    if (g->dim == 2) return g->rows * g->n;
+    return g->rows * g->n * g->n;
+}
+
+static bool grid_ok(const ek_grid* g) {
+    if (!g) {
+        set_error("null grid");
+        return false;
+    }
+    if (g->n < 1 || g->rows < 1 || g->ncomp < 1 || g->ncomp > 2 || g->dim < 1 || g->dim > 3) {
+        set_error("invalid grid (n=%lld rows=%lld ncomp=%d dim=%d)", (long long)g->n,
+                  (long long)g->rows, g->ncomp, g->dim);
+        return false;
+    }
+    return true;
+}
+
+constexpr int RPT2 = 4;  // rows per thread (2-D march)
+constexpr int RPT3 = 4;  // planes per thread (3-D march)
+
+static dim3 stencil_grid(const ek_grid* g) {
+    if (g->dim == 3)
+        return dim3((unsigned)((g->n + 31) / 32), (unsigned)((g->n + 7) / 8),
+                    (unsigned)((g->rows + RPT3 - 1) / RPT3));
+    return dim3((unsigned)((g->n + 31) / 32), (unsigned)((g->rows + 8 * RPT2 - 1) / (8 * RPT2)), 1);
+}
+
+static int64_t stencil_blocks(const ek_grid* g) {
+    dim3 d = stencil_grid(g);
+    return (int64_t)d.x * d.y * d.z;
+}
+
+template <class P, int EV, int EP>
+static int launch_p(const KArgs& a, cudaStream_t s) {
+    const dim3 blk(32, 8, 1);
+    const dim3 grd = stencil_grid(&a.g);
+    if constexpr (P::DIM == 3) {
+        k_stencil3d<P, EV, EP, RPT3><<<grd, blk, 0, s>>>(a);
+    } else {
+        k_stencil2d<P, EV, EP, RPT2><<<grd, blk, 0, s>>>(a);
+    }
+    EK_LAUNCH_CHECK("stencil launch");
+    return EK_OK;
+}
+
+// Valid (problem, value) pairs; EV_LIN only for linear problems, EV_BURGJ /
+// EV_REMBURG only for Burgers.
+template <class P, int EP>
+static int launch_ev(int ev, const KArgs& a, cudaStream_t s) {
+    switch (ev) {
+        case EV_RHS:
+            if constexpr (EP == EP_STORE) return launch_p<P, EV_RHS, EP>(a, s);
+            break;
+        case EV_FD:
+            if constexpr (EP != EP_REM) return launch_p<P, EV_FD, EP>(a, s);
+            break;
+        case EV_LIN:
+            if constexpr (P::LINEAR && EP != EP_REM) return launch_p<P, EV_LIN, EP>(a, s);
+            break;
+        case EV_BURGJ:
+            if constexpr (std::is_same<P, PBurgers>::value && EP != EP_REM)
+                return launch_p<P, EV_BURGJ, EP>(a, s);
+            break;
+        case EV_REMFD:
+            if constexpr (EP == EP_REM) return launch_p<P, EV_REMFD, EP>(a, s);
+            break;
+        case EV_REMLIN:
+            if constexpr (P::LINEAR && EP == EP_REM) return launch_p<P, EV_REMLIN, EP>(a, s);
+            break;
+        case EV_REMBURG:
+            if constexpr (std::is_same<P, PBurgers>::value && EP == EP_REM)
+                return launch_p<P, EV_REMBURG, EP>(a, s);
+            break;
+    }
+    set_error("unsupported stencil pass (problem %d, value %d, epilogue %d)", a.g.problem, ev, EP);
+    return EK_ERR_UNSUPPORTED;
+}
+
+template <int EP>
+static int launch_stencil(int ev, const KArgs& a, cudaStream_t s) {
+    switch (a.g.problem) {
+        case EK_P_ADR: return launch_ev<PAdr, EP>(ev, a, s);
+        case EK_P_ALLEN_CAHN: return launch_ev<PAllenCahn, EP>(ev, a, s);
+        case EK_P_BRUSS_PRINTED: return launch_ev<PBruss<false>, EP>(ev, a, s);
+        case EK_P_BRUSS_STANDARD: return launch_ev<PBruss<true>, EP>(ev, a, s);
+        case EK_P_GRAY_SCOTT: return launch_ev<PGrayScott, EP>(ev, a, s);
+        case EK_P_ADVDIFF2D: return launch_ev<PAdvDiff2, EP>(ev, a, s);
+        case EK_P_BURGERS2D: return launch_ev<PBurgers, EP>(ev, a, s);
+        case EK_P_ADVDIFF3D: return launch_ev<PAdvDiff3, EP>(ev, a, s);
+    }
+    set_error("problem %d has no 2-D/3-D stencil", a.g.problem);
+    return EK_ERR_UNSUPPORTED;
+}
+
+static void base_args(KArgs& a, const ek_grid* g, const double* const* halo) {
+    memset(&a, 0, sizeof(a));
+    a.g = *g;
+    a.npts = grid_points(g);
+    if (halo) {
+        a.hu = halo[0];
+        a.hy = halo[1];
+        a.hk = halo[2];
+    }
+}
+
+// analytic Jacobian value kind of a problem
+static int analytic_ev(const ek_grid* g) {
+    if (g->problem == EK_P_ADVDIFF2D || g->problem == EK_P_ADVDIFF3D) return EV_LIN;
+    if (g->problem == EK_P_BURGERS2D) return EV_BURGJ;
+    return -1;
+}
+
+static int jv_ev(const ek_grid* g, int jac) {
+    if (jac == EK_JAC_FD) return EV_FD;
+    const int ev = analytic_ev(g);
+    if (ev < 0) set_error("problem %d has no analytic Jacobian stencil", g->problem);
+    return ev;
+}
+
+}  // namespace ek
+
+using namespace ek;
+
+// =============================================================== C ABI
+extern "C" {
+
+const char* ek_last_error(void) { return g_err; }
+int ek_version(void) { return 1; }
+
+int ek_copy(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
+    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                           : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, k, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "ek_copy");
+    return EK_OK;
+}
+
+int ek_sync(void* stream) {
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "ek_sync");
+    return EK_OK;
+}
+
+int64_t ek_grid_len(const ek_grid* g) {
+    if (!g) return 0;
+    if (g->problem == EK_P_SEMILINEAR) return g->n + 1;
+    return (int64_t)g->ncomp * grid_points(g);
+}
+
+int64_t ek_workspace_bytes(const ek_grid* g) {
+    int64_t nb = VGRID_MAX;
+    if (g && g->dim >= 2) {
+        const int64_t sb = stencil_blocks(g);
+        if (sb > nb) nb = sb;
+    }
+    return nb * 8 * (int64_t)sizeof(double);
+}
+
+int ek_rhs(const ek_grid* g, const double* u, double* out, const double* const* halo,
+           void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (g->problem == EK_P_SEMILINEAR) {
+        SemiArgs a{};
+        a.n = g->n; a.h = g->h; a.h2 = g->h2; a.h24 = g->prm[0];
+        a.mode = 0; a.u = u; a.out = out;
+        k_semilinear<<<1, TPB, 0, s>>>(a);
+        EK_LAUNCH_CHECK("k_semilinear");
+        return EK_OK;
+    }
+    KArgs a;
+    base_args(a, g, halo);
+    a.u = u;
+    a.out = out;
+    return launch_stencil<EP_STORE>(EV_RHS, a, s);
+}
+
+int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu, const double* v,
+          double eps, double* out, ek_scalar_state* st, double* work,
+          const double* const* halo, void* stream) {
+    (void)work;
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (g->problem == EK_P_SEMILINEAR) {
+        SemiArgs a{};
+        a.n = g->n; a.h = g->h; a.h2 = g->h2; a.h24 = g->prm[0];
+        a.mode = jac == EK_JAC_FD ? 1 : 2;
+        a.u = u; a.y = v; a.fu = fu; a.eps = eps; a.out = out; a.st = st;
+        k_semilinear<<<1, TPB, 0, s>>>(a);
+        EK_LAUNCH_CHECK("k_semilinear");
+        return EK_OK;
+    }
+    const int ev = jv_ev(g, jac);
+    if (ev < 0) return EK_ERR_UNSUPPORTED;
+    KArgs a;
+    base_args(a, g, halo);
+    a.u = u; a.fu = fu; a.y = v; a.eps = eps; a.out = out;
+    int rc = launch_stencil<EP_STORE>(ev, a, s);
+    if (rc != EK_OK || jac != EK_JAC_FD || !st) return rc;
+    // non-finite check of the FD result (linalg.py:127-128)
+    k_norm2<<<vgrid(ek_grid_len(g)), TPB, 0, s>>>(ek_grid_len(g), out, nullptr, st, 6, work);
+    EK_LAUNCH_CHECK("k_norm2");
+    return EK_OK;
+}
+
+int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu, const double* k,
+                 double eps, double* out, ek_scalar_state* st, double* work, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (g->problem == EK_P_SEMILINEAR) {
+        set_error("semilinear remainder runs through the generic path");
+        return EK_ERR_UNSUPPORTED;
+    }
+    int ev;
+    if (jac == EK_JAC_FD) ev = EV_REMFD;
+    else if (analytic_ev(g) == EV_LIN) ev = EV_REMLIN;
+    else if (analytic_ev(g) == EV_BURGJ) ev = EV_REMBURG;
+    else {
+        set_error("problem %d has no analytic Jacobian stencil", g->problem);
+        return EK_ERR_UNSUPPORTED;
+    }
+    KArgs a;
+    base_args(a, g, nullptr);
+    a.u = u; a.fu = fu; a.k = k; a.eps = eps; a.out = out; a.st = st; a.work = work;
+    return launch_stencil<EP_REM>(ev, a, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------- Leja
+// m = 0 over a flat vector of length len (the state block must hold tol,
+// nu and k; see ek_leja_state).
+int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
+                      const double* coef_dev, ek_leja_state* st, double* work, void* stream) {
+    if (k < 1 || k > 8 || len < 1) {
+        set_error("ek_leja_begin_len: bad k=%d len=%lld", k, (long long)len);
+        return EK_ERR_INVALID;
+    }
+    LejaVArgs a{};
+    a.len = len; a.b = b; a.nk = k; a.coef = coef_dev; a.mi = 0; a.m = 0; a.st = st; a.work = work;
+    for (int q = 0; q < k; ++q) a.p[q] = p[q];
+    k_leja_begin<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
+    EK_LAUNCH_CHECK("k_leja_begin");
+    return EK_OK;
+}
+
+int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu, const double* b,
+                double* const* ybuf, double* const* p, int k, const double* coef_dev,
+                int chunk_base, int m_begin, int m_end, double gamma, ek_leja_state* st,
+                double* work, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (k < 1 || k > 8) {
+        set_error("ek_leja_run: k=%d out of range", k);
+        return EK_ERR_INVALID;
+    }
+    const int ev = jv_ev(g, jac);
+    if (ev < 0) return EK_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    KArgs a;
+    base_args(a, g, nullptr);
+    a.u = u; a.fu = fu; a.nk = k; a.coef = coef_dev; a.gamma = gamma; a.st = st; a.work = work;
+    for (int q = 0; q < k; ++q) a.p[q] = p[q];
+    for (int m = m_begin; m < m_end; ++m) {
+        a.m = m;
+        a.mi = m - chunk_base;
+        a.y = (m == 1) ? b : ybuf[(m - 1) & 1];
+        a.out = ybuf[m & 1];
+        const int rc = launch_stencil<EP_LEJA>(ev, a, s);
+        if (rc != EK_OK) return rc;
+    }
+    return EK_OK;
+}
+
+int ek_leja_update(int64_t len, const double* jv, const double* y, double* ynext,
+                   double* const* p, int k, const double* coef_dev, int chunk_base, int m,
+                   double gamma, int check_jv, ek_leja_state* st, double* work, void* stream) {
+    (void)check_jv;
+    if (k < 1 || k > 8) {
+        set_error("ek_leja_update: k=%d out of range", k);
+        return EK_ERR_INVALID;
+    }
+    LejaVArgs a{};
+    a.len = len; a.b = jv; a.y = y; a.ynext = ynext; a.nk = k; a.coef = coef_dev;
+    a.mi = m - chunk_base; a.m = m; a.gamma = gamma; a.st = st; a.work = work;
+    for (int q = 0; q < k; ++q) a.p[q] = p[q];
+    k_leja_update<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
+    EK_LAUNCH_CHECK("k_leja_update");
+    return EK_OK;
+}
+
+// ------------------------------------------------------------------ power
+int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, const double* v0,
+                 double* const* wbuf, int it_begin, int it_end, ek_power_state* st,
+                 double* work, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    const int ev = jv_ev(g, jac);
+    if (ev < 0) return EK_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t len = ek_grid_len(g);
+    if (it_begin == 0) {
+        // v = v0 / ||v0||   (spectrum.py:49-51): divisor and, for FD, ||v||
+        k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, v0, 0, st, work);
+        EK_LAUNCH_CHECK("k_power_norm");
+        if (jac == EK_JAC_FD) {
+            k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, v0, 1, st, work);
+            EK_LAUNCH_CHECK("k_power_norm");
+        }
+    }
+    KArgs a;
+    base_args(a, g, nullptr);
+    a.u = u; a.fu = fu; a.st = st; a.work = work;
+    for (int it = it_begin; it < it_end; ++it) {
+        a.y = it == 0 ? v0 : wbuf[(it - 1) & 1];
+        a.out = wbuf[it & 1];
+        const int rc = launch_stencil<EP_POWER>(ev, a, s);
+        if (rc != EK_OK) return rc;
+        if (jac == EK_JAC_FD) {
+            k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, a.out, 1, st, work);
+            EK_LAUNCH_CHECK("k_power_norm");
+        }
+    }
+    return EK_OK;
+}
+
+// ------------------------------------------------------------------ KIOPS
+int ek_arnoldi_init(int64_t n, int p, const double* src, const double* tail_host, double* V0,
+                    ek_arnoldi_state* st, double* work, void* stream) {
+    if (p < 0 || p > 5) {
+        set_error("ek_arnoldi_init: p=%d out of range", p);
+        return EK_ERR_INVALID;
+    }
+    ArnVArgs a{};
+    a.n = n; a.p = p; a.src = src; a.w = V0; a.st = st; a.work = work;
+    for (int t = 0; t < p; ++t) a.tail0[t] = tail_host[t];
+    cudaStream_t s = (cudaStream_t)stream;
+    k_arn_init<<<vgrid(n), TPB, 0, s>>>(a);
+    EK_LAUNCH_CHECK("k_arn_init");
+    a.jj = 0;
+    k_arn_scale<<<vgrid(n + p), TPB, 0, s>>>(a);
+    EK_LAUNCH_CHECK("k_arn_scale");
+    return EK_OK;
+}
+
+static void arn_window(ArnVArgs& a, double* const* V, int jj, int iop) {
+    const int lo = jj - iop > 0 ? jj - iop : 0;
+    a.nwin = jj - lo;
+    for (int q = 0; q < a.nwin; ++q) a.win[q] = V[lo + q];
+}
+
+int ek_arnoldi_run(const ek_grid* g, int jac, const double* u, const double* fu,
+                   double* const* V, const double* const* aug, const int* aug_tail, int naug,
+                   double aug_scale, int j_begin, int j_end, double* H, ek_arnoldi_state* st, int p, int iop,
+                   int ldh, double dt, double* work, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (iop < 1 || iop > 4 || p < 1 || p > 5 || naug > 5) {
+        set_error("ek_arnoldi_run: iop=%d p=%d naug=%d out of range", iop, p, naug);
+        return EK_ERR_INVALID;
+    }
+    const int ev = jv_ev(g, jac);
+    if (ev < 0) return EK_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = ek_grid_len(g);
+    KArgs a;
+    base_args(a, g, nullptr);
+    a.u = u; a.fu = fu; a.st = st; a.work = work; a.H = H; a.ldh = ldh; a.dt = dt;
+    a.n_aug = p; a.naug = naug; a.aug_scale = aug_scale;
+    for (int t = 0; t < naug; ++t) {
+        a.aug[t] = aug[t];
+        a.aug_tail[t] = aug_tail[t];
+    }
+    ArnVArgs b{};
+    b.n = n; b.p = p; b.H = H; b.ldh = ldh; b.st = st; b.work = work;
+    for (int jj = j_begin + 1; jj <= j_end; ++jj) {
+        ArnVArgs w{};
+        arn_window(w, V, jj, iop);
+        a.nwin = w.nwin;
+        for (int q = 0; q < 4; ++q) a.win[q] = w.win[q];
+        a.jj = jj;
+        a.y = V[jj - 1];
+        a.out = V[jj];
+        int rc = launch_stencil<EP_ARN>(ev, a, s);
+        if (rc != EK_OK) return rc;
+        b.nwin = w.nwin;
+        for (int q = 0; q < 4; ++q) b.win[q] = w.win[q];
+        b.jj = jj;
+        b.w = V[jj];
+        k_arn_orth<<<vgrid(n + p), TPB, 0, s>>>(b);
+        EK_LAUNCH_CHECK("k_arn_orth");
+        k_arn_scale<<<vgrid(n + p), TPB, 0, s>>>(b);
+        EK_LAUNCH_CHECK("k_arn_scale");
+    }
+    return EK_OK;
+}
+
+int ek_arnoldi_augment(int64_t n, int p, const double* jv, double* const* V, int jj, int iop,
+                       const double* const* aug, const int* aug_tail, int naug, double aug_scale,
+                       double* H, int ldh,
+                       ek_arnoldi_state* st, double* work, void* stream) {
+    if (iop < 1 || iop > 4 || p < 1 || p > 5 || naug > 5) {
+        set_error("ek_arnoldi_augment: iop=%d p=%d naug=%d out of range", iop, p, naug);
+        return EK_ERR_INVALID;
+    }
+    ArnVArgs a{};
+    a.n = n; a.p = p; a.jv = jv; a.H = H; a.ldh = ldh; a.st = st; a.work = work; a.jj = jj;
+    a.naug = naug; a.aug_scale = aug_scale;
+    for (int t = 0; t < naug; ++t) {
+        a.aug[t] = aug[t];
+        a.aug_tail[t] = aug_tail[t];
+    }
+    arn_window(a, V, jj, iop);
+    a.w = V[jj];
+    k_arn_augment<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(a);
+    EK_LAUNCH_CHECK("k_arn_augment");
+    return EK_OK;
+}
+
+int ek_arnoldi_orth(int64_t n, int p, double* const* V, int jj, int iop, double* H, int ldh,
+                    ek_arnoldi_state* st, double* work, void* stream) {
+    ArnVArgs a{};
+    a.n = n; a.p = p; a.H = H; a.ldh = ldh; a.st = st; a.work = work; a.jj = jj;
+    arn_window(a, V, jj, iop);
+    a.w = V[jj];
+    cudaStream_t s = (cudaStream_t)stream;
+    k_arn_orth<<<vgrid(n + p), TPB, 0, s>>>(a);
+    EK_LAUNCH_CHECK("k_arn_orth");
+    k_arn_scale<<<vgrid(n + p), TPB, 0, s>>>(a);
+    EK_LAUNCH_CHECK("k_arn_scale");
+    return EK_OK;
+}
+
+int ek_basis_combine(int64_t n, double* const* V, const double* coef_host, int j, double* out,
+                     void* stream) {
+    if (j < 1 || j > MAXB) {
+        set_error("ek_basis_combine: j=%d out of range", j);
+        return EK_ERR_INVALID;
+    }
+    CombineArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n = n; a.j = j; a.out = out;
+    for (int i = 0; i < j; ++i) {
+        a.rows[i] = V[i];
+        a.coef[i] = coef_host[i];
+    }
+    k_basis_combine<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(a);
+    EK_LAUNCH_CHECK("k_basis_combine");
+    return EK_OK;
+}
+
+// ---------------------------------------------------------------- vectors
+int ek_vexpr(int64_t len, const int32_t* prog, int nprog, const double* scal, int nscal,
+             const double* const* in, int nin, double* const* out, int nout,
+             ek_scalar_state* st, double* work, void* stream) {
+    if (nprog < 1 || nprog > VX_MAXPROG || nscal > 16 || nin > 8 || nout > 4) {
+        set_error("ek_vexpr: program too large (nprog=%d nscal=%d nin=%d nout=%d)", nprog,
+                  nscal, nin, nout);
+        return EK_ERR_INVALID;
+    }
+    VexprArgs a;
+    memset(&a, 0, sizeof(a));
+    a.len = len; a.nprog = nprog; a.st = st; a.work = work;
+    int reduce = 0;
+    for (int i = 0; i < nprog; ++i) {
+        a.prog[i] = prog[i];
+        const int op = prog[i] & 0xff;
+        if (op == VX_NORM || op == VX_CHECK || op == VX_ACC) reduce = 1;
+    }
+    if (reduce && (!st || !work)) {
+        set_error("ek_vexpr: reducing program needs a state block and workspace");
+        return EK_ERR_INVALID;
+    }
+    a.reduce = reduce;
+    for (int i = 0; i < nscal; ++i) a.scal[i] = scal[i];
+    for (int i = 0; i < nin; ++i) a.in[i] = in[i];
+    for (int i = 0; i < nout; ++i) a.out[i] = out[i];
+    k_vexpr<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
+    EK_LAUNCH_CHECK("k_vexpr");
+    return EK_OK;
+}
+
+int ek_norm2(int64_t len, const double* x, ek_scalar_state* st, int slot, double* work,
+             void* stream) {
+    if (slot < 0 || slot > 6) {
+        set_error("ek_norm2: slot %d", slot);
+        return EK_ERR_INVALID;
+    }
+    k_norm2<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(len, x, nullptr, st, slot, work);
+    EK_LAUNCH_CHECK("k_norm2");
+    return EK_OK;
+}
+
+int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot, double* work,
+          void* stream) {
+    k_l1<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(len, x, st, slot, work);
+    EK_LAUNCH_CHECK("k_l1");
+    return EK_OK;
+}
+
+int ek_dense_gemv(int64_t n, const double* A, const double* x, double* y, void* stream) {
+    const int64_t warps = n;
+    const int64_t blocks = (warps * 32 + TPB - 1) / TPB;
+    k_dense_gemv<<<(unsigned)blocks, TPB, 0, (cudaStream_t)stream>>>(n, A, x, y);
+    EK_LAUNCH_CHECK("k_dense_gemv");
+    return EK_OK;
+}
+
+}  // extern "C"

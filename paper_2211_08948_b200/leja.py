@@ -1,0 +1,249 @@
+"""Real-Leja interpolation of phi-function actions on the GPU.
+
+Drop-in for `expkit.leja` (leja.py:1-189). Host side (unchanged semantics):
+the Leja point sequence and its text cache, and the divided differences at
+the Leja points (first column of phi_l of a bidiagonal node matrix, scipy
+`expm` — BASELINE.json north_star keeps them on the host). Device side: the
+Newton-Leja recurrence.
+
+For a native stencil Jacobian every iteration is ONE fused kernel
+(`ek_leja_run`): the Jacobian stencil (FD or analytic), the shifted/scaled
+recurrence y' = J y / gamma - (c/gamma + xi[m-1]) y, all k polynomial
+accumulators p_i += d_i[m] y', the deterministic ||y'||^2 reduction and the
+per-coefficient freeze test |d_i[m]| ||y'|| < tol — decided on the device
+with the reference's own fp64 expression. The host uploads one 32-column
+coefficient chunk at a time (the reference recomputes its divided
+differences per 32-point chunk, leja.py:168-171) and synchronises once per
+launch batch, never per iteration.
+"""
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .errors import NonConvergence
+from .linalg import MatrixFreeOperator, dense_phi_action, fused_target
+from .spectrum import SpectrumEstimate
+
+DEFAULT_NUM_POINTS = 400
+DEFAULT_CANDIDATES = 100_000
+_CHUNK = 32
+
+_cached_points = None
+
+
+def generate_leja_points(m=DEFAULT_NUM_POINTS, n_candidates=DEFAULT_CANDIDATES):
+    """Greedy Leja sequence on [-2, 2] from xi_0 = 2 (leja.py:32-50): each
+    point maximises the log-product of distances on a uniform candidate grid,
+    ties toward the smaller candidate."""
+    if m < 1:
+        raise ValueError("need at least one point")
+    cand = np.linspace(-2.0, 2.0, n_candidates)
+    pts = np.empty(m)
+    pts[0] = 2.0
+    with np.errstate(divide="ignore"):
+        score = np.log(np.abs(cand - pts[0]))
+        for k in range(1, m):
+            pts[k] = cand[int(np.argmax(score))]
+            score += np.log(np.abs(cand - pts[k]))
+    return pts
+
+
+def _default_cache_path():
+    root = os.environ.get("XDG_CACHE_HOME") or str(Path.home() / ".cache")
+    return Path(root) / "expkit" / "leja_points.txt"
+
+
+def get_leja_points(m=DEFAULT_NUM_POINTS, cache_path=None):
+    """Leja points from the in-process / text cache (leja.py:58-76); the
+    text format (%.17g per line) round-trips exactly."""
+    global _cached_points
+    if _cached_points is not None and len(_cached_points) >= m:
+        return _cached_points[:m]
+    path = Path(cache_path) if cache_path is not None else _default_cache_path()
+    if path.exists():
+        pts = np.loadtxt(path, ndmin=1)
+        if len(pts) >= m:
+            _cached_points = pts
+            return pts[:m]
+    pts = generate_leja_points(max(m, DEFAULT_NUM_POINTS))
+    try:
+        path.parent.mkdir(parents=True, exist_ok=True)
+        np.savetxt(path, pts, fmt="%.17g")
+    except OSError:
+        pass
+    _cached_points = pts
+    return pts[:m]
+
+
+@dataclass(frozen=True)
+class DividedDifferences:
+    d: np.ndarray
+    l: int
+    h: float
+    c: float
+    gamma: float
+
+
+def divided_differences(l, h, est: SpectrumEstimate, xi, m_max):
+    """Newton divided differences of z -> phi_l(h (c + gamma z)) at xi[:m_max]
+    (leja.py:88-111), read off the first column of phi_l of the lower
+    bidiagonal matrix diag(h (c + gamma xi)) + h gamma * subdiag."""
+    if not 0 <= l <= 4:
+        raise ValueError("phi order must be in 0..4")
+    if h < 0:
+        raise ValueError("scale h must be >= 0")
+    m_max = min(m_max, len(xi))
+    L = np.diag(h * (est.c + est.gamma * xi[:m_max]))
+    r = np.arange(m_max - 1)
+    L[r + 1, r] = h * est.gamma
+    e1 = np.zeros(m_max)
+    e1[0] = 1.0
+    d = dense_phi_action(l, L, e1)
+    if not np.isfinite(d).all():
+        raise NonConvergence("non-finite divided differences; spectral estimate invalid")
+    return DividedDifferences(d=d, l=l, h=h, c=est.c, gamma=est.gamma)
+
+
+@dataclass
+class LejaResult:
+    vectors: list
+    iters: int
+    freeze_iters: list
+
+
+def leja_interpolate(J: MatrixFreeOperator, b, l, h, est, tol,
+                     xi=None, max_points=DEFAULT_NUM_POINTS):
+    """p ~ phi_l(h J) b; returns (p, iters) (leja.py:121-130)."""
+    res = leja_interpolate_vertical(J, b, l, [1.0], h, est, tol,
+                                    xi=xi, max_points=max_points)
+    return res.vectors[0], res.iters
+
+
+class _CoefTable:
+    """(k+1) x 32 device table of one chunk: row 0 the shifts
+    c/gamma + xi[m-1] (Python-evaluated, leja.py:172), rows 1..k the divided
+    differences d_i[m]."""
+
+    def __init__(self, k):
+        self.k = k
+        self.dev = D.empty((k + 1) * _CHUNK)
+        self.host = np.zeros((k + 1) * _CHUNK)
+
+    def load(self, base, hi, dds, c, gamma, xi):
+        h = self.host
+        h[:] = 0.0
+        for m in range(base, hi):
+            col = m - base
+            if m >= 1:
+                h[col] = c / gamma + xi[m - 1]
+            for i, d in enumerate(dds):
+                h[(1 + i) * _CHUNK + col] = d[m]
+        N.check(N.lib().ek_copy(C.c_void_p(self.dev.data_ptr()),
+                                h.ctypes.data_as(C.c_void_p), h.nbytes, 1, D.stream()),
+                "coef upload")
+
+
+def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
+                              xi=None, max_points=DEFAULT_NUM_POINTS):
+    """phi_l(c_i h J) b for several scale factors c_i sharing one Newton
+    basis recurrence (leja.py:133-189). Accumulator i freezes once
+    |d_i[m]| ||y_m|| < tol; the loop runs until all are frozen.
+
+    Returns LejaResult(vectors, iters, freeze_iters); raises NonConvergence
+    after `max_points` terms or on a non-finite ||y||."""
+    if tol <= 0:
+        raise ValueError("tolerance must be positive")
+    if len(coeffs) < 1:
+        raise ValueError("need at least one coefficient")
+    for ci in coeffs:
+        if not 0.0 < ci <= 1.0:
+            raise ValueError("coefficients must lie in (0, 1]")
+    if len(coeffs) > 8:
+        raise ValueError("at most 8 coefficients per vertical group")
+    if xi is None:
+        xi = get_leja_points(max_points)
+    k = len(coeffs)
+    c, gamma = est.c, est.gamma
+    bd = D.to_dev(b)
+    n = bd.numel()
+    if n != J.dim:
+        raise ValueError(f"expected vector of length {J.dim}, got {n}")
+
+    m_avail = min(_CHUNK, max_points)
+    dds = [divided_differences(l, ci * h, est, xi, m_avail).d for ci in coeffs]
+    table = _CoefTable(k)
+    table.load(0, min(_CHUNK, m_avail), dds, c, gamma, xi)
+
+    fused = fused_target(J)
+    if fused is not None and (fused[1] != 1.0 or fused[0].grid.problem == N.P_SEMILINEAR):
+        fused = None
+    Jn = fused[0] if fused else None
+    nu = Jn.nu if Jn is not None and Jn.jac == N.JAC_FD else 0.0
+
+    ps = [D.empty(n) for _ in range(k)]
+    st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k)
+    ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(Jn.grid)) if Jn else None)
+    pp = N.ptrs(ps)
+    N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()), pp, k,
+                                      C.c_void_p(table.dev.data_ptr()), st.ptr, ws,
+                                      D.stream()), "ek_leja_begin_len")
+    hst = st.read()
+    if hst.done:
+        return LejaResult(vectors=[D.like_input(p, b) for p in ps], iters=0,
+                          freeze_iters=[0] * k)
+
+    ybuf = [D.empty(n), D.empty(n)]
+    yp = N.ptrs(ybuf)
+    fd_seen = 0
+    m = 1
+    base = 0
+    while m < max_points:
+        if m >= m_avail:  # next 32-point chunk (leja.py:168-171)
+            m_avail = min(m_avail + _CHUNK, max_points)
+            dds = [divided_differences(l, ci * h, est, xi, m_avail).d for ci in coeffs]
+            base = m
+            table.load(base, m_avail, dds, c, gamma, xi)
+        if Jn is not None:
+            # launch batch: short first batch (most calls finish early), then
+            # the rest of the chunk; kernels after termination early-exit
+            hi = min(m_avail, m + 8) if m == 1 else m_avail
+            N.check(N.lib().ek_leja_run(
+                C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
+                C.c_void_p(Jn.fu.data_ptr()), C.c_void_p(bd.data_ptr()), yp, pp, k,
+                C.c_void_p(table.dev.data_ptr()), base, m, hi, float(gamma), st.ptr,
+                ws, D.stream()), "ek_leja_run")
+            hst = st.read()
+            if Jn.jac == N.JAC_FD:
+                Jn.rhs.counter.charge(hst.fd_evals - fd_seen)
+                fd_seen = hst.fd_evals
+        else:
+            # generic operator: its action runs elsewhere, one sync per step
+            hi = m + 1
+            y = bd if m == 1 else ybuf[(m - 1) & 1]
+            jv = J.apply_dev(y)
+            N.check(N.lib().ek_leja_update(
+                n, C.c_void_p(jv.data_ptr()), C.c_void_p(y.data_ptr()),
+                C.c_void_p(ybuf[m & 1].data_ptr()), pp, k,
+                C.c_void_p(table.dev.data_ptr()), base, m, float(gamma), 0, st.ptr,
+                ws, D.stream()), "ek_leja_update")
+            hst = st.read()
+        if hst.status == N.ST_JV_NONFINITE:
+            raise FloatingPointError("non-finite Jacobian action")
+        if hst.status == N.ST_NORM_NONFINITE:
+            raise NonConvergence("polynomial iteration diverged", iters=int(hst.iters))
+        if hst.done:
+            return LejaResult(vectors=[D.like_input(p, b) for p in ps],
+                              iters=int(hst.iters),
+                              freeze_iters=[int(hst.freeze[i]) for i in range(k)])
+        m = hi
+
+    stalled = [coeffs[i] for i in range(k) if (hst.active >> i) & 1]
+    raise NonConvergence(
+        f"no convergence in {max_points} Leja points",
+        iters=max_points, detail={"stalled_coefficients": stalled})
