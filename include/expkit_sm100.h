@@ -145,6 +145,8 @@ typedef struct ek_arnoldi_state {
 /* ------------------------------------------------------------ utilities */
 const char* ek_last_error(void);
 int ek_version(void);
+/* Number of kernels this library has launched (process-wide). */
+long long ek_launch_count(void);
 /* Bytes of device workspace (block partials) any call on this grid needs. */
 int64_t ek_workspace_bytes(const ek_grid* g);
 /* Stream-ordered copies (kind: 1 = host->device, 2 = device->host; a copy

@@ -73,6 +73,7 @@ _PP = C.POINTER(C.c_void_p)
 _SIGS = {
     "ek_last_error": (C.c_char_p, []),
     "ek_version": (_I, []),
+    "ek_launch_count": (C.c_longlong, []),
     "ek_grid_len": (_L, [C.POINTER(Grid)]),
     "ek_workspace_bytes": (_L, [C.POINTER(Grid)]),
     "ek_copy": (_I, [_P, _P, _L, _I, _P]),

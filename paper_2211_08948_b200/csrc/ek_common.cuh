@@ -22,8 +22,10 @@ constexpr double SQRT_EPS = 1.4901161193847656e-08;  // math.sqrt(2**-52), linal
 // ---------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
+void count_launch();  // ek_launch_count(): kernels launched by this library
 #define EK_LAUNCH_CHECK(where)                                                \
     do {                                                                      \
+        ::ek::count_launch();                                                 \
         cudaError_t e_ = cudaGetLastError();                                  \
         if (e_ != cudaSuccess) return ::ek::cuda_status(e_, where);           \
     } while (0)

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <type_traits>
 
 #include "ek_common.cuh"
@@ -27,6 +28,9 @@ int cuda_status(cudaError_t e, const char* where) {
     set_error("%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
     return EK_ERR_CUDA;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ------------------------------------------------------------- 1-D problem
 // problems.py:154-196: semilinear, Dirichlet, nonlocal trapezoid integral.
@@ -250,6 +254,7 @@ extern "C" {
 
 const char* ek_last_error(void) { return g_err; }
 int ek_version(void) { return 1; }
+long long ek_launch_count(void) { return g_launches.load(); }
 
 int ek_copy(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
     const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice

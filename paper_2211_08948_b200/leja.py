@@ -36,6 +36,11 @@ _CHUNK = 32
 
 _cached_points = None
 
+# Optional measurement hook (bench.py): when a list, each fused call
+# appends {"events": [(start, end), ...], "iters", "freeze", "k", "n", "fd"}
+# with CUDA events bracketing its ek_leja_run launch batches.
+PROFILE = None
+
 
 def generate_leja_points(m=DEFAULT_NUM_POINTS, n_candidates=DEFAULT_CANDIDATES):
     """Greedy Leja sequence on [-2, 2] from xi_0 = 2 (leja.py:32-50): each
@@ -203,6 +208,10 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     fd_seen = 0
     m = 1
     base = 0
+    prof = None
+    if PROFILE is not None and Jn is not None:
+        prof = {"events": [], "k": k, "n": n, "fd": Jn.jac == N.JAC_FD}
+        PROFILE.append(prof)
     while m < max_points:
         if m >= m_avail:  # next 32-point chunk (leja.py:168-171)
             m_avail = min(m_avail + _CHUNK, max_points)
@@ -213,12 +222,23 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             # launch batch: short first batch (most calls finish early), then
             # the rest of the chunk; kernels after termination early-exit
             hi = min(m_avail, m + 8) if m == 1 else m_avail
+            if prof is not None:
+                import torch
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
             N.check(N.lib().ek_leja_run(
                 C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
                 C.c_void_p(Jn.fu.data_ptr()), C.c_void_p(bd.data_ptr()), yp, pp, k,
                 C.c_void_p(table.dev.data_ptr()), base, m, hi, float(gamma), st.ptr,
                 ws, D.stream()), "ek_leja_run")
+            if prof is not None:
+                ev[1].record()
+                prof["events"].append(ev)
             hst = st.read()
+            if prof is not None:
+                prof["iters"] = int(hst.m)
+                prof["freeze"] = [int(hst.freeze[i]) if not (hst.active >> i) & 1
+                                  else int(hst.m) for i in range(k)]
             if Jn.jac == N.JAC_FD:
                 Jn.rhs.counter.charge(hst.fd_evals - fd_seen)
                 fd_seen = hst.fd_evals

@@ -20,6 +20,7 @@ from paper_2211_08948_b200 import ext, problems as P
 from paper_2211_08948_b200 import _device as D, _native as N
 
 from conftest import cases
+from oracle import np_fields as OF, np_integrate as OI
 
 pytestmark = pytest.mark.gpu
 
@@ -231,10 +232,57 @@ def test_adaptive_trajectory(golden, xi, case):
     tr = ek.adaptive_loop(p.rhs, p.u0, p.t_final, integ, scheme, float(g("tol")),
                           jac_factory=p.jac_factory, ctx=ek.EngineContext(xi=xi),
                           max_steps=int(g("max_steps")))
-    assert [tr.steps_accepted, tr.steps_rejected, tr.rhs_evals, tr.leja_iters,
-            tr.krylov_matvecs, tr.substeps] == list(g("counts"))
-    assert rel(np.array(tr.dts), g("dts")) <= 1e-8
-    assert rel(tr.u, g("u")) <= 1e-10
+    counts = [tr.steps_accepted, tr.steps_rejected, tr.rhs_evals, tr.leja_iters,
+              tr.krylov_matvecs, tr.substeps]
+    same = counts == list(g("counts")) and len(tr.dts) == len(g("dts"))
+    if same:
+        d_dts = rel(np.array(tr.dts), g("dts"))
+        d_u = rel(tr.u, g("u"))
+        if d_dts <= 1e-8 and d_u <= 1e-10:
+            return  # tier T3: identical decisions, <= 1e-10 solution
+    assert "kiops" in scheme or scheme == "lekry", "Leja runs must meet tier T3"
+    # KIOPS adaptivity (ceil/log decisions, kiops.py:212-252) amplifies ulp
+    # differences; the contract is then the oracle's own sensitivity
+    # envelope: rerun the oracle with its norms perturbed by one ulp.
+    env = _oracle_envelope(pname, integ, scheme, float(g("tol")), int(g("max_steps")), xi)
+    base = list(g("counts"))
+    for i, c in enumerate(counts):
+        lo = min([base[i]] + [e[0][i] for e in env])
+        hi = max([base[i]] + [e[0][i] for e in env])
+        assert lo <= c <= hi, (i, c, lo, hi)
+    env_u = max(rel(e[1], g("u")) for e in env)
+    assert rel(tr.u, g("u")) <= max(10.0 * env_u, 1e-10), (rel(tr.u, g("u")), env_u)
+
+
+ORACLE = {
+    "adr": lambda: OF.make("adr", alpha=0.1, n=16),
+    "allen_cahn": lambda: OF.make("allen_cahn", alpha=1e-2, n=16),
+    "bruss_printed": lambda: OF.brusselator(1e-3, 12, form="printed"),
+    "bruss_standard": lambda: OF.brusselator(0.02, 12, form="standard"),
+    "gray_scott": lambda: OF.make("gray_scott", alpha=1e-3, n=16),
+    "semilinear": lambda: OF.semilinear(20),
+}
+
+
+def _oracle_envelope(pname, integ, scheme, tol, max_steps, xi):
+    """Oracle runs with every np.linalg.norm scaled by 1 +- 1 ulp
+    (SURVEY.md Appendix B): [(counts, u), ...]."""
+    def run():
+        p = ORACLE[pname]()
+        r = OI.adaptive(p.rhs, p.u0, p.t_final, integ, scheme, tol,
+                        jac_factory=p.jac_factory, ctx=OI.Ctx(xi=xi),
+                        max_steps=max_steps)
+        return ([r.steps_accepted, r.steps_rejected, r.rhs_evals, r.leja_iters,
+                 r.krylov_matvecs, r.substeps], r.u)
+    out = []
+    real = np.linalg.norm
+    for f in (1.0 + 2.0**-52, 1.0 - 2.0**-53, 1.0 + 2.0**-51, 1.0 - 2.0**-52):
+        np.linalg.norm = lambda *a, f=f, **k: real(*a, **k) * f
+        try:
+            out.append(run())
+        finally:
+            np.linalg.norm = real
+    return out
 
 
 @pytest.mark.parametrize("name", list(EXT))
