@@ -268,6 +268,10 @@ int ek_norm2(int64_t len, const double* x, ek_scalar_state* st, int slot,
 /* sum |x| -> st->val[slot]  (kiops.py:146). */
 int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot,
           double* work, void* stream);
+/* Self test of the division used by the kernels: fast[i] = reciprocal-
+ * correction quotient, exact[i] = x[i]/d[i] by the division instruction. */
+int ek_selftest_div(int64_t n, const double* x, const double* d, double* fast,
+                    double* exact, void* stream);
 /* y = A x, A dense row-major (linalg.py:87-90 from_matrix). */
 int ek_dense_gemv(int64_t n, const double* A, const double* x, double* y,
                   void* stream);

@@ -100,6 +100,7 @@ _SIGS = {
                       _PP, _I, _P, _P, _P]),
     "ek_norm2": (_I, [_L, _P, _P, _I, _P, _P]),
     "ek_l1": (_I, [_L, _P, _P, _I, _P, _P]),
+    "ek_selftest_div": (_I, [_L, _P, _P, _P, _P, _P]),
     "ek_dense_gemv": (_I, [_L, _P, _P, _P, _P]),
 }
 

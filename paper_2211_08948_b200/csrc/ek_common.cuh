@@ -102,6 +102,20 @@ __device__ __forceinline__ void gather_partials(const double* work, long nb, dou
     block_sum<NQ>(tot);
 }
 
+// Division by a launch-uniform divisor: reciprocal r = RN(1/d) plus one
+// exact-residual correction, q = x r; q += (x - q d) r. Returns the
+// correctly rounded IEEE quotient (checked against the division
+// instruction on the device by tests/test_gpu_kernels.py).
+struct Dv {
+    double d, r;  // divisor and RN(1/d)
+};
+__host__ __device__ __forceinline__ Dv mkdv(double d) { return Dv{d, 1.0 / d}; }
+__device__ __forceinline__ double dv(double x, const Dv& c) {
+    const double q = __dmul_rn(x, c.r);
+    const double e = fma(-q, c.d, x);
+    return fma(e, c.r, q);
+}
+
 // x^3 with a double-double intermediate: the correctly rounded cube in all
 // but vanishingly rare cases, which is what NumPy's pow(x, 3) returns
 // (problems.py:94 `f**3`).

@@ -18,18 +18,25 @@
 //     EP_ARN     w = dt*value + tail@uflip ; window dots (kiops.py:182-187)
 //     EP_REM     out = value ; non-finite flag (integrators.py:107-108)
 //
-// Geometry: axis 0 (i, slowest; the slab axis) is marched by each thread
-// over RPT consecutive rows/planes held in registers, so the vertical
-// neighbours are re-used instead of re-loaded; the contiguous axis is one
-// warp lane per column (coalesced 256-B row segments) with the +-1
-// neighbours exchanged by warp shuffles; in 3-D the middle axis comes from
-// the block's other warps through L1. Ghost rows follow the boundary
-// condition: reflect (np.pad 'reflect', Neumann), wrap (periodic), or the
-// halo buffers of a slab (multi-GPU).
+// Geometry: a warp owns 32 consecutive columns of the contiguous axis (one
+// lane per column, coalesced 256-B segments) and marches RPT consecutive
+// rows of axis 0 (the slab axis) held in registers, so vertical neighbours
+// are reused. Horizontal neighbours come from warp shuffles; lanes 0 and 1
+// load the two halo columns of the warp. In 3-D the middle axis comes from
+// the neighbouring warps through L1. Every input of a tile (neighbourhood
+// rows, centre values, accumulators) is loaded before the first store, so a
+// thread keeps ~(RPT+2)*NC*NCH + RPT*NC*(K+2) independent loads in flight.
+// Blocks are persistent (grid = SMs x occupancy) and walk the tiles.
+// Ghost rows follow the boundary condition: reflect (np.pad 'reflect',
+// Neumann), wrap (periodic), or the halo buffers of a slab (multi-GPU).
 //
-// Arithmetic: every expression is written in NumPy's evaluation order and the
-// library is compiled with -fmad=false, so values match the reference's
-// elementwise results bit for bit (given identical inputs).
+// Arithmetic: every expression follows NumPy's evaluation order and the
+// library is compiled with -fmad=false. Divisions by launch-uniform values
+// (h**2, 2h, h, eps, gamma, ||w||) use the reciprocal r = RN(1/d) with one
+// exact-residual correction, q = x r; q += (x - q d) r (two FMAs), which
+// returns the correctly rounded IEEE quotient x/d (verified on the device
+// against the division instruction, tests/test_gpu_kernels.py), at a third
+// of the cost of a division call.
 #pragma once
 
 #include "ek_common.cuh"
@@ -50,34 +57,40 @@ struct Nb {
     double c, xm, xp, ym, yp, zm, zp;  // centre, axis0 -/+, axis1 -/+, axis2 -/+
 };
 
+// Problem constants of one launch.
+struct PC {
+    Dv h2, two_h, h;
+    double prm[8];
+};
+
 // ------------------------------------------------------------------ physics
 
-__device__ __forceinline__ double lap2(const Nb& s, double h2) {
-    return ((((s.xm + s.xp) + s.ym) + s.yp) - 4.0 * s.c) / h2;  // problems.py:28-29
+__device__ __forceinline__ double lap2(const Nb& s, const PC& g) {
+    return dv((((s.xm + s.xp) + s.ym) + s.yp) - 4.0 * s.c, g.h2);  // problems.py:28-29
 }
-__device__ __forceinline__ double lap3(const Nb& s, double h2) {
-    return ((((((s.xm + s.xp) + s.ym) + s.yp) + s.zm) + s.zp) - 6.0 * s.c) / h2;
+__device__ __forceinline__ double lap3(const Nb& s, const PC& g) {
+    return dv(((((s.xm + s.xp) + s.ym) + s.yp) + s.zm) + s.zp - 6.0 * s.c, g.h2);
 }
 // one-sided difference following the sign of +v.grad u (forward for v >= 0)
-__device__ __forceinline__ double upw_x(const Nb& s, double v, double h) {
-    return v >= 0.0 ? (s.xp - s.c) / h : (s.c - s.xm) / h;
+__device__ __forceinline__ double upw_x(const Nb& s, double v, const PC& g) {
+    return v >= 0.0 ? dv(s.xp - s.c, g.h) : dv(s.c - s.xm, g.h);
 }
-__device__ __forceinline__ double upw_y(const Nb& s, double v, double h) {
-    return v >= 0.0 ? (s.yp - s.c) / h : (s.c - s.ym) / h;
+__device__ __forceinline__ double upw_y(const Nb& s, double v, const PC& g) {
+    return v >= 0.0 ? dv(s.yp - s.c, g.h) : dv(s.c - s.ym, g.h);
 }
-__device__ __forceinline__ double upw_z(const Nb& s, double v, double h) {
-    return v >= 0.0 ? (s.zp - s.c) / h : (s.c - s.zm) / h;
+__device__ __forceinline__ double upw_z(const Nb& s, double v, const PC& g) {
+    return v >= 0.0 ? dv(s.zp - s.c, g.h) : dv(s.c - s.zm, g.h);
 }
 
 // problems.py:69-83. prm: alpha, beta, gamma
 struct PAdr {
     static constexpr int NC = 1, DIM = 2;
     static constexpr bool LINEAR = false;
-    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const PC& g) {
         const Nb& q = s[0];
-        const double lap = lap2(q, g.h2);
-        const double gx = (q.xp - q.xm) / g.two_h;
-        const double gy = (q.yp - q.ym) / g.two_h;
+        const double lap = lap2(q, g);
+        const double gx = dv(q.xp - q.xm, g.two_h);
+        const double gy = dv(q.yp - q.ym, g.two_h);
         const double grad = gx + gy;
         const double c = q.c;
         o[0] = ((g.prm[0] * lap) + (g.prm[1] * grad)) + (((g.prm[2] * c) * (1.0 - c)) * (c - 0.5));
@@ -88,8 +101,8 @@ struct PAdr {
 struct PAllenCahn {
     static constexpr int NC = 1, DIM = 2;
     static constexpr bool LINEAR = false;
-    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
-        o[0] = ((g.prm[0] * lap2(s[0], g.h2)) + s[0].c) - cube_cr(s[0].c);
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const PC& g) {
+        o[0] = ((g.prm[0] * lap2(s[0], g)) + s[0].c) - cube_cr(s[0].c);
     }
 };
 
@@ -98,12 +111,12 @@ template <bool STD>
 struct PBruss {
     static constexpr int NC = 2, DIM = 2;
     static constexpr bool LINEAR = false;
-    __device__ static void f(const Nb (&s)[2], double (&o)[2], const ek_grid& g) {
+    __device__ static void f(const Nb (&s)[2], double (&o)[2], const PC& g) {
         const double u = s[0].c, v = s[1].c;
         const double uu_v = (u * u) * v;
         const double react = STD ? uu_v : u * (v * v);
-        o[0] = (((g.prm[0] * lap2(s[0], g.h2)) + react) - (4.0 * u)) + 1.0;
-        o[1] = ((g.prm[0] * lap2(s[1], g.h2)) - uu_v) + (3.0 * u);
+        o[0] = (((g.prm[0] * lap2(s[0], g)) + react) - (4.0 * u)) + 1.0;
+        o[1] = ((g.prm[0] * lap2(s[1], g)) - uu_v) + (3.0 * u);
     }
 };
 
@@ -111,11 +124,11 @@ struct PBruss {
 struct PGrayScott {
     static constexpr int NC = 2, DIM = 2;
     static constexpr bool LINEAR = false;
-    __device__ static void f(const Nb (&s)[2], double (&o)[2], const ek_grid& g) {
+    __device__ static void f(const Nb (&s)[2], double (&o)[2], const PC& g) {
         const double u = s[0].c, v = s[1].c;
         const double uvv = u * (v * v);
-        o[0] = ((g.prm[0] * lap2(s[0], g.h2)) - uvv) + (g.prm[1] * (1.0 - u));
-        o[1] = ((g.prm[0] * lap2(s[1], g.h2)) + uvv) - (g.prm[2] * v);
+        o[0] = ((g.prm[0] * lap2(s[0], g)) - uvv) + (g.prm[1] * (1.0 - u));
+        o[1] = ((g.prm[0] * lap2(s[1], g)) + uvv) - (g.prm[2] * v);
     }
 };
 
@@ -123,10 +136,10 @@ struct PGrayScott {
 struct PAdvDiff2 {
     static constexpr int NC = 1, DIM = 2;
     static constexpr bool LINEAR = true;
-    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const PC& g) {
         const Nb& q = s[0];
-        o[0] = ((g.prm[0] * lap2(q, g.h2)) + (g.prm[1] * upw_x(q, g.prm[1], g.h)))
-               + (g.prm[2] * upw_y(q, g.prm[2], g.h));
+        o[0] = ((g.prm[0] * lap2(q, g)) + (g.prm[1] * upw_x(q, g.prm[1], g)))
+               + (g.prm[2] * upw_y(q, g.prm[2], g));
     }
 };
 
@@ -134,17 +147,17 @@ struct PAdvDiff2 {
 struct PBurgers {
     static constexpr int NC = 1, DIM = 2;
     static constexpr bool LINEAR = false;
-    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const PC& g) {
         const Nb& q = s[0];
-        const double gx = ((q.xp * q.xp) - (q.xm * q.xm)) / g.two_h;
-        const double gy = ((q.yp * q.yp) - (q.ym * q.ym)) / g.two_h;
-        o[0] = ((g.prm[0] * lap2(q, g.h2)) + (0.5 * gx)) + (0.5 * gy);
+        const double gx = dv((q.xp * q.xp) - (q.xm * q.xm), g.two_h);
+        const double gy = dv((q.yp * q.yp) - (q.ym * q.ym), g.two_h);
+        o[0] = ((g.prm[0] * lap2(q, g)) + (0.5 * gx)) + (0.5 * gy);
     }
     // J(u) v = eta Lap v + d_x(u v) + d_y(u v)
-    __device__ static double jac(const Nb& u, const Nb& v, const ek_grid& g) {
-        const double gx = ((u.xp * v.xp) - (u.xm * v.xm)) / g.two_h;
-        const double gy = ((u.yp * v.yp) - (u.ym * v.ym)) / g.two_h;
-        return ((g.prm[0] * lap2(v, g.h2)) + gx) + gy;
+    __device__ static double jac(const Nb& u, const Nb& v, const PC& g) {
+        const double gx = dv((u.xp * v.xp) - (u.xm * v.xm), g.two_h);
+        const double gy = dv((u.yp * v.yp) - (u.ym * v.ym), g.two_h);
+        return ((g.prm[0] * lap2(v, g)) + gx) + gy;
     }
 };
 
@@ -152,11 +165,11 @@ struct PBurgers {
 struct PAdvDiff3 {
     static constexpr int NC = 1, DIM = 3;
     static constexpr bool LINEAR = true;
-    __device__ static void f(const Nb (&s)[1], double (&o)[1], const ek_grid& g) {
+    __device__ static void f(const Nb (&s)[1], double (&o)[1], const PC& g) {
         const Nb& q = s[0];
-        o[0] = (((g.prm[0] * lap3(q, g.h2)) + (g.prm[1] * upw_x(q, g.prm[1], g.h)))
-                + (g.prm[2] * upw_y(q, g.prm[2], g.h)))
-               + (g.prm[3] * upw_z(q, g.prm[3], g.h));
+        o[0] = (((g.prm[0] * lap3(q, g)) + (g.prm[1] * upw_x(q, g.prm[1], g)))
+                + (g.prm[2] * upw_y(q, g.prm[2], g)))
+               + (g.prm[3] * upw_z(q, g.prm[3], g));
     }
 };
 
@@ -164,6 +177,7 @@ struct PAdvDiff3 {
 
 struct KArgs {
     ek_grid g;
+    PC pc;
     long npts;            // points per component (local)
     long n_aug;           // length of the tail (KIOPS p), 0 otherwise
     // raw fields, component-major
@@ -182,7 +196,7 @@ struct KArgs {
     int m;                // iteration index
     int jj;               // Arnoldi: index of the vector being built
     const double* coef;   // Leja table: row 0 shift, rows 1..k d_i (32 wide)
-    double gamma;
+    Dv gamma;
     double eps;           // host-provided FD increment (EP_STORE / EP_REM)
     double dt;            // Arnoldi: operator scale (A.scaled(dt))
     void* st;             // state block (type depends on the epilogue)
@@ -207,7 +221,8 @@ __device__ __forceinline__ long wrap_idx(long i, long n, int bc) {
     return i < 0 ? 1 : n - 2;  // np.pad 'reflect': mirror without repeating the edge
 }
 
-// Base of row (2-D) / plane (3-D) `i` of component c of a field, i in [-1, rows].
+// Offset of row (2-D) / plane (3-D) `i` of component c inside a field, or of
+// its copy in the halo buffer; i in [-1, rows].
 __device__ __forceinline__ const double* slab_row(const KArgs& a, const double* base,
                                                   const double* halo, int c, long i,
                                                   long rowlen) {
@@ -220,7 +235,8 @@ __device__ __forceinline__ const double* slab_row(const KArgs& a, const double* 
 // Scalars a kernel reads from its state block before the sweep.
 struct Ctl {
     double eps;
-    double ydiv;          // power iteration: v = w / ||w||
+    Dv eps_d;
+    Dv ydiv;              // power iteration: v = w / ||w||
     bool has_div;
     uint32_t active;
     double shift;
@@ -229,8 +245,7 @@ struct Ctl {
     double augc[5];       // Arnoldi: tail[aug_tail[t]] * nu (exact: nu = 2^-e)
 };
 
-// Gather the channel values of one grid point (element pointer offsets are
-// per field because a ghost row may live in a halo buffer).
+// Channel values of one grid point.
 template <int EV, int NCH>
 __device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const double* py,
                                       const double* pk, long e, double (&ch)[NCH]) {
@@ -238,15 +253,15 @@ __device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const do
         ch[0] = __ldg(pu + e);
     } else if constexpr (EV == EV_FD) {
         double yv = __ldg(py + e);
-        if (ctl.has_div) yv = yv / ctl.ydiv;
+        if (ctl.has_div) yv = dv(yv, ctl.ydiv);
         ch[0] = __ldg(pu + e) + ctl.eps * yv;  // u + eps*v   (linalg.py:126)
     } else if constexpr (EV == EV_LIN) {
         double yv = __ldg(py + e);
-        if (ctl.has_div) yv = yv / ctl.ydiv;
+        if (ctl.has_div) yv = dv(yv, ctl.ydiv);
         ch[0] = yv;
     } else if constexpr (EV == EV_BURGJ) {
         double yv = __ldg(py + e);
-        if (ctl.has_div) yv = yv / ctl.ydiv;
+        if (ctl.has_div) yv = dv(yv, ctl.ydiv);
         ch[0] = __ldg(pu + e);
         ch[1] = yv;
     } else if constexpr (EV == EV_REMFD) {
@@ -266,73 +281,68 @@ __device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const do
     }
 }
 
-// Value at the centre from the channel neighbourhoods.
+// Value at the centre from the channel neighbourhoods; fuc = f(u_n) there.
 template <class P, int EV, int NCH>
 __device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
-                                         const Nb (&nb)[P::NC][NCH], long off,
-                                         double (&val)[P::NC]) {
+                                         const Nb (&nb)[P::NC][NCH],
+                                         const double (&fuc)[P::NC], double (&val)[P::NC]) {
     constexpr int NC = P::NC;
     if constexpr (EV == EV_RHS || EV == EV_LIN) {
         Nb s[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) s[c] = nb[c][0];
-        P::f(s, val, a.g);
+        P::f(s, val, a.pc);
     } else if constexpr (EV == EV_FD) {
         Nb s[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) s[c] = nb[c][0];
         double fw[NC];
-        P::f(s, fw, a.g);
+        P::f(s, fw, a.pc);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const double fuc = __ldg(a.fu + c * a.npts + off);
-            val[c] = ctl.y_zero ? 0.0 : (fw[c] - fuc) / ctl.eps;  // linalg.py:126
-        }
+        for (int c = 0; c < NC; ++c)
+            val[c] = ctl.y_zero ? 0.0 : dv(fw[c] - fuc[c], ctl.eps_d);  // linalg.py:126
     } else if constexpr (EV == EV_BURGJ) {
-        if constexpr (NC == 1 && NCH == 2) {
-            val[0] = PBurgers::jac(nb[0][0], nb[0][1], a.g);
-        }
+        if constexpr (NC == 1 && NCH == 2) val[0] = PBurgers::jac(nb[0][0], nb[0][1], a.pc);
     } else if constexpr (EV == EV_REMFD) {
         Nb s0[NC], s1[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) { s0[c] = nb[c][0]; s1[c] = nb[c][1]; }
         double fk[NC], fw[NC];
-        P::f(s0, fk, a.g);
-        P::f(s1, fw, a.g);
+        P::f(s0, fk, a.pc);
+        P::f(s1, fw, a.pc);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const double fn = __ldg(a.fu + c * a.npts + off);
-            val[c] = (fk[c] - fn) - ((fw[c] - fn) / ctl.eps);  // integrators.py:106
-        }
+        for (int c = 0; c < NC; ++c)
+            val[c] = (fk[c] - fuc[c]) - dv(fw[c] - fuc[c], ctl.eps_d);  // integrators.py:106
     } else if constexpr (EV == EV_REMLIN) {
         Nb s0[NC], s1[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) { s0[c] = nb[c][0]; s1[c] = nb[c][1]; }
         double fk[NC], jd[NC];
-        P::f(s0, fk, a.g);
-        P::f(s1, jd, a.g);
+        P::f(s0, fk, a.pc);
+        P::f(s1, jd, a.pc);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const double fn = __ldg(a.fu + c * a.npts + off);
-            val[c] = (fk[c] - fn) - jd[c];
-        }
+        for (int c = 0; c < NC; ++c) val[c] = (fk[c] - fuc[c]) - jd[c];
     } else {  // EV_REMBURG
         if constexpr (NC == 1 && NCH == 3) {
             Nb s0[1] = {nb[0][0]};
             double fk[1];
-            P::f(s0, fk, a.g);
-            const double fn = __ldg(a.fu + off);
-            val[0] = (fk[0] - fn) - PBurgers::jac(nb[0][1], nb[0][2], a.g);
+            P::f(s0, fk, a.pc);
+            val[0] = (fk[0] - fuc[0]) - PBurgers::jac(nb[0][1], nb[0][2], a.pc);
         }
     }
+}
+
+template <int EV>
+__host__ __device__ constexpr bool needs_fu() {
+    return EV == EV_FD || EV == EV_REMFD || EV == EV_REMLIN || EV == EV_REMBURG;
 }
 
 // Read the state scalars; false = the iteration has already terminated.
 template <int EV, int EP>
 __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     ctl.eps = a.eps;
-    ctl.ydiv = 1.0;
     ctl.has_div = false;
+    ctl.ydiv = Dv{1.0, 1.0};
     ctl.active = 0u;
     ctl.shift = 0.0;
     ctl.y_zero = false;
@@ -348,7 +358,7 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     } else if constexpr (EP == EP_POWER) {
         const ek_power_state* st = (const ek_power_state*)a.st;
         if (st->done || st->status) return false;
-        ctl.ydiv = st->nw;  // v = w / ||w|| of the previous iterate
+        ctl.ydiv = mkdv(st->nw);  // v = w / ||w|| of the previous iterate
         ctl.has_div = true;
         ctl.eps = (SQRT_EPS * (1.0 + st->nu)) / st->nv;
     } else if constexpr (EP == EP_ARN) {
@@ -361,13 +371,40 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
         for (int t = 0; t < 5; ++t)
             ctl.augc[t] = t < a.naug ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
     }
+    ctl.eps_d = mkdv(ctl.eps);
     return true;
 }
 
+// Centre values loaded with the neighbourhood, before any store.
+template <int EV, int EP, int NC, int K>
+struct Centre {
+    double fu[NC];
+    double y[NC];
+    double p[K > 0 ? K : 1][NC];
+};
+
+template <int EV, int EP, int NC, int K>
+__device__ __forceinline__ void load_centre(const KArgs& a, const Ctl& ctl, long off,
+                                            Centre<EV, EP, NC, K>& z) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const long e = c * a.npts + off;
+        if constexpr (needs_fu<EV>()) z.fu[c] = __ldg(a.fu + e);
+        else z.fu[c] = 0.0;
+        if constexpr (EP == EP_LEJA) {
+            z.y[c] = __ldg(a.y + e);
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                z.p[q][c] = ((ctl.active >> q) & 1u) ? a.p[q][e] : 0.0;
+        }
+    }
+}
+
 // Per-point epilogue; acc[] collects this thread's partial reductions.
-template <int EV, int EP, int NC>
+template <int EV, int EP, int NC, int K>
 __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long off,
-                                         const double (&val)[NC], double* acc) {
+                                         const double (&val)[NC],
+                                         const Centre<EV, EP, NC, K>& z, double* acc) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         const long e = c * a.npts + off;
@@ -376,16 +413,14 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             a.out[e] = v;
         } else if constexpr (EP == EP_LEJA) {
             // y = J.apply(y)/gamma - (c/gamma + xi[m-1]) * y      leja.py:172
-            const double yn = (v / a.gamma) - (ctl.shift * __ldg(a.y + e));
+            const double yn = dv(v, a.gamma) - (ctl.shift * z.y[c]);
             a.out[e] = yn;
             acc[0] += yn * yn;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (q < a.nk && ((ctl.active >> q) & 1u)) {
-                    double* pq = a.p[q];
-                    pq[e] = pq[e] + (ctl.d[q] * yn);  // ps[i] + dds[i][m]*y  leja.py:179
-                }
+            for (int q = 0; q < K; ++q) {
+                if ((ctl.active >> q) & 1u)
+                    a.p[q][e] = z.p[q][c] + (ctl.d[q] * yn);  // ps[i] + dds[i][m]*y  leja.py:179
             }
         } else if constexpr (EP == EP_POWER) {
             a.out[e] = v;
@@ -399,7 +434,9 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
                 if (t < a.naug) augv = augv + (ctl.augc[t] * __ldg(a.aug[t] + e));
             const double w = (a.dt * v) + augv;
             a.out[e] = w;
-            for (int q = 0; q < a.nwin; ++q) acc[q] += __ldg(a.win[q] + e) * w;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < a.nwin) acc[q] += __ldg(a.win[q] + e) * w;
             if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
         } else {  // EP_REM
             a.out[e] = v;
@@ -412,29 +449,55 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
 template <int EV, int EP>
 __device__ void finalize(const KArgs& a, const double* tot);
 
-// ------------------------------------------------------------ 2-D kernel
+template <int EP>
+__device__ __forceinline__ uint32_t* ticket_of(const KArgs& a) {
+    if constexpr (EP == EP_LEJA) return &((ek_leja_state*)a.st)->ticket;
+    else if constexpr (EP == EP_POWER) return &((ek_power_state*)a.st)->ticket;
+    else if constexpr (EP == EP_ARN) return &((ek_arnoldi_state*)a.st)->ticket;
+    else return &((ek_scalar_state*)a.st)->ticket;
+}
 
-template <class P, int EV, int EP, int RPT>
+template <int EV, int EP, int NQ>
+__device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc)[NQ]) {
+    if constexpr (ep_nq(EP) > 0) {
+        block_sum<NQ>(acc);
+        if (publish_and_arrive<NQ>(acc, a.work, ticket_of<EP>(a))) {
+            double tot[NQ];
+            gather_partials<NQ>(a.work, nblocks(), tot);
+            if (flat_tid() == 0) finalize<EV, EP>(a, tot);
+        }
+    }
+}
+
+// ------------------------------------------------------------ 2-D kernel
+// Tile = 32 columns x (8 warps * RPT rows); 1-D blocks of 256 threads.
+
+template <class P, int EV, int EP, int RPT, int K>
 __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
-    const int lane = threadIdx.x, ty = threadIdx.y;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const long cols = a.g.n, rows = a.g.rows;
-    const long j = (long)blockIdx.x * 32 + lane;
-    const long i0 = ((long)blockIdx.y * 8 + ty) * RPT;
-    const long jc = j < cols ? j : cols - 1;
+    const long tiles_c = (cols + 31) / 32;
+    const long tile_rows = 8L * RPT;
+    const long ntiles = tiles_c * ((rows + tile_rows - 1) / tile_rows);
     double acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
-    if (i0 < rows) {  // warp-uniform
-        const long jw = wrap_idx(jc - 1, cols, a.g.bc);
-        const long je = wrap_idx(jc + 1, cols, a.g.bc);
-        const bool needW = lane == 0;
-        const bool needE = lane == 31 || jc == cols - 1;
+    for (long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const long j0 = (t % tiles_c) * 32;
+        const long i0 = (t / tiles_c) * tile_rows + (long)wid * RPT;
+        const long j = j0 + lane;
+        const long jc = j < cols ? j : cols - 1;
+        const int elane = (int)(cols - 1 - j0 < 31 ? cols - 1 - j0 : 31);
+        // lane 0 holds the west halo column of the warp, lane 1 the east one
+        const long hcol = lane == 0 ? wrap_idx(j0 - 1, cols, a.g.bc)
+                                    : wrap_idx(j0 + elane + 1, cols, a.g.bc);
         double cv[RPT + 2][NC][NCH];
-        double cw[RPT][NC][NCH], ce[RPT][NC][NCH];
+        double hv[RPT][NC][NCH];
+        Centre<EV, EP, NC, K> zc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT + 2; ++r) {
             long i = i0 - 1 + r;
@@ -446,10 +509,19 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
                 const double* pk = slab_row(a, a.k, a.hk, c, i, cols);
                 fetch<EV, NCH>(ctl, pu, py, pk, jc, cv[r][c]);
                 if (r >= 1 && r <= RPT) {
-                    if (needW) fetch<EV, NCH>(ctl, pu, py, pk, jw, cw[r - 1][c]);
-                    if (needE) fetch<EV, NCH>(ctl, pu, py, pk, je, ce[r - 1][c]);
+                    if (lane < 2) fetch<EV, NCH>(ctl, pu, py, pk, hcol, hv[r - 1][c]);
+                    else {
+#pragma unroll
+                        for (int h = 0; h < NCH; ++h) hv[r - 1][c][h] = 0.0;
+                    }
                 }
             }
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            long i = i0 + r;
+            if (i >= rows) i = rows - 1;
+            load_centre<EV, EP, NC, K>(a, ctl, i * cols + jc, zc[r]);
         }
 #pragma unroll
         for (int r = 1; r <= RPT; ++r) {
@@ -462,8 +534,10 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
                     const double cc = cv[r][c][h];
                     double w = __shfl_up_sync(0xffffffffu, cc, 1);
                     double e = __shfl_down_sync(0xffffffffu, cc, 1);
-                    if (needW) w = cw[r - 1][c][h];
-                    if (needE) e = ce[r - 1][c][h];
+                    const double hw = __shfl_sync(0xffffffffu, hv[r - 1][c][h], 0);
+                    const double he = __shfl_sync(0xffffffffu, hv[r - 1][c][h], 1);
+                    if (lane == 0) w = hw;
+                    if (lane == elane) e = he;
                     nb[c][h].c = cc;
                     nb[c][h].xm = cv[r - 1][c][h];
                     nb[c][h].xp = cv[r + 1][c][h];
@@ -474,54 +548,46 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
                 }
             }
             if (i < rows && j < cols) {
-                const long off = i * cols + j;
                 double val[NC];
-                evaluate<P, EV, NCH>(a, ctl, nb, off, val);
-                epilogue<EV, EP, NC>(a, ctl, off, val, acc);
+                evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val);
+                epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, zc[r - 1], acc);
             }
         }
     }
-    if constexpr (ep_nq(EP) > 0) {
-        block_sum<NQ>(acc);
-        uint32_t* ticket = nullptr;
-        if constexpr (EP == EP_LEJA) ticket = &((ek_leja_state*)a.st)->ticket;
-        else if constexpr (EP == EP_POWER) ticket = &((ek_power_state*)a.st)->ticket;
-        else if constexpr (EP == EP_ARN) ticket = &((ek_arnoldi_state*)a.st)->ticket;
-        else ticket = &((ek_scalar_state*)a.st)->ticket;
-        if (publish_and_arrive<NQ>(acc, a.work, ticket)) {
-            double tot[NQ];
-            gather_partials<NQ>(a.work, nblocks(), tot);
-            if (flat_tid() == 0) finalize<EV, EP>(a, tot);
-        }
-    }
+    reduce_and_finalize<EV, EP, NQ>(a, acc);
 }
 
 // ------------------------------------------------------------ 3-D kernel
-// lanes along k (axis 2), threadIdx.y along j (axis 1), RPT planes of i.
+// Tile = 32 (k, contiguous) x 8 (j, one per warp) x RPT planes (i).
 
-template <class P, int EV, int EP, int RPT>
+template <class P, int EV, int EP, int RPT, int K>
 __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
-    const int lane = threadIdx.x, ty = threadIdx.y;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const long n = a.g.n, rows = a.g.rows, plane = n * n;
-    const long kx = (long)blockIdx.x * 32 + lane;
-    const long jy = (long)blockIdx.y * 8 + ty;
-    const long i0 = (long)blockIdx.z * RPT;
-    const long kc = kx < n ? kx : n - 1;
+    const long tk = (n + 31) / 32, tj = (n + 7) / 8, ti = (rows + RPT - 1) / RPT;
+    const long ntiles = tk * tj * ti;
     double acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
-    if (i0 < rows && jy < n) {  // warp-uniform
-        const long kw = wrap_idx(kc - 1, n, a.g.bc), ke = wrap_idx(kc + 1, n, a.g.bc);
-        const long jm = wrap_idx(jy - 1, n, a.g.bc), jp = wrap_idx(jy + 1, n, a.g.bc);
-        const bool needW = lane == 0;
-        const bool needE = lane == 31 || kc == n - 1;
+    for (long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const long k0 = (t % tk) * 32;
+        const long jy = ((t / tk) % tj) * 8 + wid;
+        const long i0 = (t / (tk * tj)) * RPT;
+        const long kx = k0 + lane;
+        const long kc = kx < n ? kx : n - 1;
+        const long jc = jy < n ? jy : n - 1;
+        const int elane = (int)(n - 1 - k0 < 31 ? n - 1 - k0 : 31);
+        const long hcol = lane == 0 ? wrap_idx(k0 - 1, n, a.g.bc)
+                                    : wrap_idx(k0 + elane + 1, n, a.g.bc);
+        const long jm = wrap_idx(jc - 1, n, a.g.bc), jp = wrap_idx(jc + 1, n, a.g.bc);
         double cv[RPT + 2][NC][NCH];
         double cjm[RPT][NC][NCH], cjp[RPT][NC][NCH];
-        double cw[RPT][NC][NCH], ce[RPT][NC][NCH];
+        double hv[RPT][NC][NCH];
+        Centre<EV, EP, NC, K> zc[RPT];
 #pragma unroll
         for (int r = 0; r < RPT + 2; ++r) {
             long i = i0 - 1 + r;
@@ -531,14 +597,23 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
                 const double* pu = slab_row(a, a.u, a.hu, c, i, plane);
                 const double* py = slab_row(a, a.y, a.hy, c, i, plane);
                 const double* pk = slab_row(a, a.k, a.hk, c, i, plane);
-                fetch<EV, NCH>(ctl, pu, py, pk, jy * n + kc, cv[r][c]);
+                fetch<EV, NCH>(ctl, pu, py, pk, jc * n + kc, cv[r][c]);
                 if (r >= 1 && r <= RPT) {
                     fetch<EV, NCH>(ctl, pu, py, pk, jm * n + kc, cjm[r - 1][c]);
                     fetch<EV, NCH>(ctl, pu, py, pk, jp * n + kc, cjp[r - 1][c]);
-                    if (needW) fetch<EV, NCH>(ctl, pu, py, pk, jy * n + kw, cw[r - 1][c]);
-                    if (needE) fetch<EV, NCH>(ctl, pu, py, pk, jy * n + ke, ce[r - 1][c]);
+                    if (lane < 2) fetch<EV, NCH>(ctl, pu, py, pk, jc * n + hcol, hv[r - 1][c]);
+                    else {
+#pragma unroll
+                        for (int h = 0; h < NCH; ++h) hv[r - 1][c][h] = 0.0;
+                    }
                 }
             }
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            long i = i0 + r;
+            if (i >= rows) i = rows - 1;
+            load_centre<EV, EP, NC, K>(a, ctl, i * plane + jc * n + kc, zc[r]);
         }
 #pragma unroll
         for (int r = 1; r <= RPT; ++r) {
@@ -551,8 +626,10 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
                     const double cc = cv[r][c][h];
                     double w = __shfl_up_sync(0xffffffffu, cc, 1);
                     double e = __shfl_down_sync(0xffffffffu, cc, 1);
-                    if (needW) w = cw[r - 1][c][h];
-                    if (needE) e = ce[r - 1][c][h];
+                    const double hw = __shfl_sync(0xffffffffu, hv[r - 1][c][h], 0);
+                    const double he = __shfl_sync(0xffffffffu, hv[r - 1][c][h], 1);
+                    if (lane == 0) w = hw;
+                    if (lane == elane) e = he;
                     nb[c][h].c = cc;
                     nb[c][h].xm = cv[r - 1][c][h];
                     nb[c][h].xp = cv[r + 1][c][h];
@@ -562,27 +639,14 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
                     nb[c][h].zp = e;
                 }
             }
-            if (i < rows && kx < n) {
-                const long off = i * plane + jy * n + kx;
+            if (i < rows && kx < n && jy < n) {
                 double val[NC];
-                evaluate<P, EV, NCH>(a, ctl, nb, off, val);
-                epilogue<EV, EP, NC>(a, ctl, off, val, acc);
+                evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val);
+                epilogue<EV, EP, NC, K>(a, ctl, i * plane + jy * n + kx, val, zc[r - 1], acc);
             }
         }
     }
-    if constexpr (ep_nq(EP) > 0) {
-        block_sum<NQ>(acc);
-        uint32_t* ticket = nullptr;
-        if constexpr (EP == EP_LEJA) ticket = &((ek_leja_state*)a.st)->ticket;
-        else if constexpr (EP == EP_POWER) ticket = &((ek_power_state*)a.st)->ticket;
-        else if constexpr (EP == EP_ARN) ticket = &((ek_arnoldi_state*)a.st)->ticket;
-        else ticket = &((ek_scalar_state*)a.st)->ticket;
-        if (publish_and_arrive<NQ>(acc, a.work, ticket)) {
-            double tot[NQ];
-            gather_partials<NQ>(a.work, nblocks(), tot);
-            if (flat_tid() == 0) finalize<EV, EP>(a, tot);
-        }
-    }
+    reduce_and_finalize<EV, EP, NQ>(a, acc);
 }
 
 // --------------------------------------------------------------- finalize

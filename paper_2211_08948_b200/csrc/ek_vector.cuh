@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(TPB) k_leja_update(const LejaVArgs a) {
     const ek_leja_state* cst = a.st;
     if (cst->done) return;
     const double shift = a.coef[a.mi];
+    const Dv gam = mkdv(a.gamma);
     const uint32_t act = cst->active;
     double d[8];
 #pragma unroll
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(TPB) k_leja_update(const LejaVArgs a) {
     double acc[1] = {0.0};
     for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
          e += (int64_t)gridDim.x * TPB) {
-        const double yn = (__ldg(a.b + e) / a.gamma) - (shift * __ldg(a.y + e));
+        const double yn = dv(__ldg(a.b + e), gam) - (shift * __ldg(a.y + e));
         a.ynext[e] = yn;
         acc[0] += yn * yn;
 #pragma unroll
@@ -298,12 +299,12 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
 __global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
     const ek_arnoldi_state* cst = a.st;
     if (cst->happy || cst->status) return;
-    const double nrm = cst->nrm;
+    const Dv nrm = mkdv(cst->nrm);
     const int64_t len = a.n + a.p;
     double acc[1] = {0.0};
     for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
          e += (int64_t)gridDim.x * TPB) {
-        const double v = a.w[e] / nrm;
+        const double v = dv(a.w[e], nrm);
         a.w[e] = v;
         if (e < a.n) acc[0] += v * v;
     }
@@ -342,12 +343,12 @@ __global__ void __launch_bounds__(TPB) k_power_norm(int64_t len, const double* _
                                                     int scaled, ek_power_state* st,
                                                     double* work) {
     if (scaled && (st->done || st->status)) return;
-    const double d = st->nw;
+    const Dv d = mkdv(st->nw);
     double acc[1] = {0.0};
     for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
          e += (int64_t)gridDim.x * TPB) {
         double v = __ldg(x + e);
-        if (scaled) v = v / d;
+        if (scaled) v = dv(v, d);
         acc[0] += v * v;
     }
     block_sum<1>(acc);
@@ -457,6 +458,21 @@ __global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
                 a.st->flag |= (tot[2] > 0.0 ? 1 : 0) | (tot[3] > 0.0 ? 2 : 0);
             }
         }
+    }
+}
+
+// --------------------------------------------------------- self test
+// fast[i] = dv(x[i], mkdv(d[i])), exact[i] = x[i] / d[i] (division
+// instruction): proves the reciprocal-correction quotient is bit-identical.
+__global__ void __launch_bounds__(TPB) k_selftest_div(int64_t n, const double* __restrict__ x,
+                                                      const double* __restrict__ d,
+                                                      double* __restrict__ fast,
+                                                      double* __restrict__ exact) {
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * TPB) {
+        const double xv = x[e], dd = d[e];
+        fast[e] = dv(xv, mkdv(dd));
+        exact[e] = xv / dd;
     }
 }
 

@@ -143,32 +143,72 @@ static bool grid_ok(const ek_grid* g) {
     return true;
 }
 
-constexpr int RPT2 = 4;  // rows per thread (2-D march)
-constexpr int RPT3 = 4;  // planes per thread (3-D march)
-
-static dim3 stencil_grid(const ek_grid* g) {
-    if (g->dim == 3)
-        return dim3((unsigned)((g->n + 31) / 32), (unsigned)((g->n + 7) / 8),
-                    (unsigned)((g->rows + RPT3 - 1) / RPT3));
-    return dim3((unsigned)((g->n + 31) / 32), (unsigned)((g->rows + 8 * RPT2 - 1) / (8 * RPT2)), 1);
+// Rows (2-D) / planes (3-D) marched per thread: keep the register footprint
+// of the neighbourhood (RPT+2)*NC*NCH and the centre values moderate.
+__host__ __device__ constexpr int rpt_for(int nc, int nch, int dim) {
+    return dim == 3 ? 2 : (nc * nch >= 2 ? 2 : 4);
 }
 
-static int64_t stencil_blocks(const ek_grid* g) {
-    dim3 d = stencil_grid(g);
-    return (int64_t)d.x * d.y * d.z;
+static int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+            n = 148;
+    }
+    return n;
+}
+
+static int64_t stencil_tiles(const ek_grid* g, int rpt) {
+    if (g->dim == 3)
+        return ((g->n + 31) / 32) * ((g->n + 7) / 8) * ((g->rows + rpt - 1) / rpt);
+    return ((g->n + 31) / 32) * ((g->rows + 8 * rpt - 1) / (8 * rpt));
+}
+
+// Persistent grid: min(tiles, SMs x resident blocks of this kernel). The
+// occupancy is cached per kernel instantiation by the caller.
+template <typename Kern>
+static unsigned persistent_grid(Kern kern, int64_t tiles, int& occ_cache) {
+    if (occ_cache == 0) {
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, 0) != cudaSuccess ||
+            occ < 1)
+            occ = 1;
+        occ_cache = occ;
+    }
+    const int64_t cap = (int64_t)sm_count() * occ_cache;
+    return (unsigned)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
+}
+
+template <class P, int EV, int EP, int K>
+static int launch_k(const KArgs& a, cudaStream_t s) {
+    constexpr int RPT = rpt_for(P::NC, ev_nch(EV), P::DIM);
+    static int occ = 0;  // one per template instantiation
+    const int64_t tiles = stencil_tiles(&a.g, RPT);
+    if constexpr (P::DIM == 3) {
+        auto kern = k_stencil3d<P, EV, EP, RPT, K>;
+        kern<<<persistent_grid(kern, tiles, occ), TPB, 0, s>>>(a);
+    } else {
+        auto kern = k_stencil2d<P, EV, EP, RPT, K>;
+        kern<<<persistent_grid(kern, tiles, occ), TPB, 0, s>>>(a);
+    }
+    EK_LAUNCH_CHECK("stencil launch");
+    return EK_OK;
 }
 
 template <class P, int EV, int EP>
 static int launch_p(const KArgs& a, cudaStream_t s) {
-    const dim3 blk(32, 8, 1);
-    const dim3 grd = stencil_grid(&a.g);
-    if constexpr (P::DIM == 3) {
-        k_stencil3d<P, EV, EP, RPT3><<<grd, blk, 0, s>>>(a);
+    if constexpr (EP == EP_LEJA) {
+        switch (a.nk) {
+            case 1: return launch_k<P, EV, EP, 1>(a, s);
+            case 2: return launch_k<P, EV, EP, 2>(a, s);
+            case 3: return launch_k<P, EV, EP, 3>(a, s);
+            default: return launch_k<P, EV, EP, 8>(a, s);
+        }
     } else {
-        k_stencil2d<P, EV, EP, RPT2><<<grd, blk, 0, s>>>(a);
+        return launch_k<P, EV, EP, 0>(a, s);
     }
-    EK_LAUNCH_CHECK("stencil launch");
-    return EK_OK;
 }
 
 // Valid (problem, value) pairs; EV_LIN only for linear problems, EV_BURGJ /
@@ -224,6 +264,11 @@ static void base_args(KArgs& a, const ek_grid* g, const double* const* halo) {
     memset(&a, 0, sizeof(a));
     a.g = *g;
     a.npts = grid_points(g);
+    a.pc.h2 = mkdv(g->h2);
+    a.pc.two_h = mkdv(g->two_h);
+    a.pc.h = mkdv(g->h);
+    for (int i = 0; i < 8; ++i) a.pc.prm[i] = g->prm[i];
+    a.gamma = mkdv(1.0);
     if (halo) {
         a.hu = halo[0];
         a.hy = halo[1];
@@ -279,7 +324,7 @@ int64_t ek_grid_len(const ek_grid* g) {
 int64_t ek_workspace_bytes(const ek_grid* g) {
     int64_t nb = VGRID_MAX;
     if (g && g->dim >= 2) {
-        const int64_t sb = stencil_blocks(g);
+        const int64_t sb = (int64_t)sm_count() * 8;  // persistent stencil grids
         if (sb > nb) nb = sb;
     }
     return nb * 8 * (int64_t)sizeof(double);
@@ -384,7 +429,7 @@ int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu, co
     cudaStream_t s = (cudaStream_t)stream;
     KArgs a;
     base_args(a, g, nullptr);
-    a.u = u; a.fu = fu; a.nk = k; a.coef = coef_dev; a.gamma = gamma; a.st = st; a.work = work;
+    a.u = u; a.fu = fu; a.nk = k; a.coef = coef_dev; a.gamma = mkdv(gamma); a.st = st; a.work = work;
     for (int q = 0; q < k; ++q) a.p[q] = p[q];
     for (int m = m_begin; m < m_end; ++m) {
         a.m = m;
@@ -618,6 +663,13 @@ int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot, double* w
           void* stream) {
     k_l1<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(len, x, st, slot, work);
     EK_LAUNCH_CHECK("k_l1");
+    return EK_OK;
+}
+
+int ek_selftest_div(int64_t n, const double* x, const double* d, double* fast, double* exact,
+                    void* stream) {
+    k_selftest_div<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(n, x, d, fast, exact);
+    EK_LAUNCH_CHECK("k_selftest_div");
     return EK_OK;
 }
 

@@ -1,0 +1,66 @@
+#!/usr/bin/env python
+"""Steady-state microbenchmark of the fused Leja iteration kernel.
+
+Runs `--iters` Leja iterations that never freeze (tol = 1e-300) on the
+periodic Brusselator (config 4 geometry) with the FD Jacobian, for k
+accumulators, and reports per-launch time and achieved algorithmic HBM
+bandwidth 8N(4+2k)/t. Used for ncu captures:
+
+  ncu --set full -k regex:k_stencil2d -s 3 -c 2 python tools/kernel_bench.py --k 1
+"""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--problem", default="brusselator_periodic")
+    args = ap.parse_args()
+
+    import torch
+    import paper_2211_08948_b200 as ek
+    from paper_2211_08948_b200 import ext, leja as L
+
+    prob = ext.make_ext_problem(args.problem, n=args.n)
+    rhs = ek.CountingRhs(prob.rhs)
+    sys_ = ek.make_linearized(rhs, prob.u0, jac_factory=prob.jac_factory)
+    lam, _ = ek.power_iterate(sys_.J)
+    est = ek.make_estimate(lam)
+    dt = 50.0 / abs(est.alpha)
+    b = ek.linalg.D.ev(ek.linalg.D.V(sys_._f) * dt)
+    coeffs = [1.0, 0.5, 0.25, 0.125][:args.k]
+    xi = ek.get_leja_points(400)
+
+    def run(iters):
+        L.PROFILE = []
+        try:
+            ek.leja_interpolate_vertical(sys_.J, b, 1, coeffs, dt, est, 1e-300, xi=xi,
+                                         max_points=iters + 1)
+        except ek.NonConvergence:
+            pass
+        torch.cuda.synchronize()
+        prof, L.PROFILE = L.PROFILE, None
+        return prof
+
+    run(4)
+    prof = run(args.iters)
+    t = sum(s.elapsed_time(e) for s, e in prof[0]["events"]) / 1e3
+    n = sys_._u.numel()
+    fd = prof[0]["fd"]
+    per = 8 * n * ((4 if fd else 2) + 2 * args.k)
+    out = {"problem": args.problem, "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
+           "ms_per_launch": t / args.iters * 1e3, "bytes_per_launch": per,
+           "GBps": per * args.iters / t / 1e9}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
