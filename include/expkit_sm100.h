@@ -147,6 +147,10 @@ const char* ek_last_error(void);
 int ek_version(void);
 /* Number of kernels this library has launched (process-wide). */
 long long ek_launch_count(void);
+/* Select the 2-D stencil implementation: 1 (default) = TMA-staged
+ * (cp.async.bulk + mbarrier pipeline), 0 = register-staged. Returns the
+ * previous setting. Both give bit-identical results. */
+int ek_set_tma(int enabled);
 /* Bytes of device workspace (block partials) any call on this grid needs. */
 int64_t ek_workspace_bytes(const ek_grid* g);
 /* Stream-ordered copies (kind: 1 = host->device, 2 = device->host; a copy

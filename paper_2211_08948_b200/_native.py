@@ -74,6 +74,7 @@ _SIGS = {
     "ek_last_error": (C.c_char_p, []),
     "ek_version": (_I, []),
     "ek_launch_count": (C.c_longlong, []),
+    "ek_set_tma": (_I, [_I]),
     "ek_grid_len": (_L, [C.POINTER(Grid)]),
     "ek_workspace_bytes": (_L, [C.POINTER(Grid)]),
     "ek_copy": (_I, [_P, _P, _L, _I, _P]),

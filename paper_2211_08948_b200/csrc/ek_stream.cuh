@@ -1,0 +1,261 @@
+// ek_stream.cuh — TMA-pipelined 2-D stencil kernel (sm_100a).
+//
+// Same value / epilogue algebra as ek_stencil.cuh, but every input tile is
+// moved by the Tensor Memory Accelerator with 2-D tensor copies
+// (`cp.async.bulk.tensor.2d`, completion counted in bytes on an mbarrier),
+// S stages deep. One thread issues a handful of box copies per chunk; the
+// data in flight lives in shared memory, not registers, so a block keeps
+// S-1 chunks (~60 KB) of HBM reads outstanding while it computes one.
+//
+// Chunk = 32 columns x 8 rows (one row per warp). Per stage:
+//   raw[f][c]  box of 10 x 36 doubles: rows r0-1..r0+8, columns j0-2..j0+33
+//              of raw neighbourhood field f (u, y or k, u), component c.
+//              The tensor map views a field as a (ncomp*rows) x cols
+//              matrix, so component c starts at row c*rows.
+//   ctr[g]     box of 8 x 32: f(u_n) / Leja accumulators at the centres.
+// Ghost rows/columns at the domain boundary (row -1 / rows, column -1 /
+// cols: wrap, reflect, or slab halo rows) are not in the boxes (TMA fills
+// them with zeros or they belong to another component); the lanes that need
+// one read it from global memory directly, so boundary conditions never
+// touch the copy engine. Requires 16-byte row pitch (even row length).
+#pragma once
+
+#include <cuda.h>
+
+#include "ek_stencil.cuh"
+
+namespace ek {
+
+constexpr int TBW = 36;          // raw box width
+constexpr int TBR = 10;          // raw box rows
+constexpr int RAW_SLOT = 368;    // doubles per raw box slot (2944 B, 128-B multiple)
+constexpr int CTR_SLOT = 256;    // 8 x 32 doubles
+constexpr int MAX_MAPS = 11;     // 2 raw + f(u) + 8 accumulators
+
+struct TmaMaps {
+    CUtensorMap m[MAX_MAPS];     // [0, nraw) raw fields, then f(u), then p_q
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra LAB_WAIT;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// raw neighbourhood fields per value kind
+template <int EV>
+__host__ __device__ constexpr int nraw() {
+    return (EV == EV_RHS || EV == EV_LIN) ? 1 : 2;
+}
+// index (within the raw fields) of y, whose centre value the Leja update needs
+template <int EV>
+__host__ __device__ constexpr int yraw() {
+    return EV == EV_LIN ? 0 : 1;
+}
+
+template <int EV, int NCH, int NR>
+__device__ __forceinline__ void make_ch(const Ctl& ctl, const double (&r)[NR], double (&ch)[NCH]) {
+    if constexpr (EV == EV_RHS) {
+        ch[0] = r[0];
+    } else if constexpr (EV == EV_FD) {
+        const double yv = ctl.has_div ? dv(r[1], ctl.ydiv) : r[1];
+        ch[0] = r[0] + ctl.eps * yv;  // u + eps*v   (linalg.py:126)
+    } else if constexpr (EV == EV_LIN) {
+        ch[0] = ctl.has_div ? dv(r[0], ctl.ydiv) : r[0];
+    } else if constexpr (EV == EV_BURGJ) {
+        ch[0] = r[0];
+        ch[1] = ctl.has_div ? dv(r[1], ctl.ydiv) : r[1];
+    } else if constexpr (EV == EV_REMFD) {
+        ch[0] = r[0];
+        ch[1] = r[1] + ctl.eps * (r[0] - r[1]);  // u + eps*(k - u)
+    } else if constexpr (EV == EV_REMLIN) {
+        ch[0] = r[0];
+        ch[1] = r[0] - r[1];
+    } else {
+        ch[0] = r[0];
+        ch[1] = r[1];
+        ch[2] = r[0] - r[1];
+    }
+}
+
+// centre maps: f(u_n) (if used) then the K accumulators
+template <int EV, int EP, int K>
+__host__ __device__ constexpr int nctr_maps() {
+    return (needs_fu<EV>() ? 1 : 0) + (EP == EP_LEJA ? K : 0);
+}
+template <int EV, int EP, int NC, int K>
+__host__ __device__ constexpr int stage_doubles() {
+    return nraw<EV>() * NC * RAW_SLOT + nctr_maps<EV, EP, K>() * NC * CTR_SLOT;
+}
+
+// Raw field base pointers (field 0 / 1) and halo buffers per value kind.
+template <int EV>
+__device__ __forceinline__ void raw_fields(const KArgs& a, const double* (&b)[2],
+                                           const double* (&h)[2]) {
+    if constexpr (EV == EV_RHS) {
+        b[0] = a.u; h[0] = a.hu; b[1] = nullptr; h[1] = nullptr;
+    } else if constexpr (EV == EV_LIN) {
+        b[0] = a.y; h[0] = a.hy; b[1] = nullptr; h[1] = nullptr;
+    } else if constexpr (EV == EV_FD || EV == EV_BURGJ) {
+        b[0] = a.u; h[0] = a.hu; b[1] = a.y; h[1] = a.hy;
+    } else {
+        b[0] = a.k; h[0] = a.hk; b[1] = a.u; h[1] = a.hu;
+    }
+}
+
+// Thread 0: expect the bytes of chunk (j0, r0) and issue its box copies.
+template <int EV, int EP, int NC, int K>
+__device__ __forceinline__ void issue_chunk(const TmaMaps& maps, double* buf, uint64_t* bar,
+                                            int j0, int r0, int rows, uint32_t active) {
+    constexpr int NR = nraw<EV>(), NCM = nctr_maps<EV, EP, K>();
+    constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    uint32_t bytes = NR * NC * (TBW * TBR * 8);
+#pragma unroll
+    for (int g = 0; g < NCM; ++g)
+        if (g < FU || ((active >> (g - FU)) & 1u)) bytes += NC * (32 * 8 * 8);
+    mbar_arrive_expect(bar, bytes);
+#pragma unroll
+    for (int f = 0; f < NR; ++f)
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            tma_load_2d(buf + (f * NC + c) * RAW_SLOT, &maps.m[f], j0 - 2, c * rows + r0 - 1, bar);
+    double* ctr = buf + NR * NC * RAW_SLOT;
+#pragma unroll
+    for (int g = 0; g < NCM; ++g) {
+        if (g < FU || ((active >> (g - FU)) & 1u)) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                tma_load_2d(ctr + (g * NC + c) * CTR_SLOT, &maps.m[NR + g], j0, c * rows + r0, bar);
+        }
+    }
+}
+
+template <class P, int EV, int EP, int K, int S>
+__global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_constant__ TmaMaps maps) {
+    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NR = nraw<EV>();
+    constexpr int SD = stage_doubles<EV, EP, NC, K>();
+    constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    extern __shared__ __align__(1024) double smem[];
+    __shared__ __align__(8) uint64_t bars[S];
+
+    Ctl ctl;
+    if (!load_ctl<EV, EP>(a, ctl)) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int cols = (int)a.g.n, rows = (int)a.g.rows;
+    const int tiles_c = (cols + 31) / 32;
+    const long nchunks = (long)tiles_c * ((rows + 7) / 8);
+    const long G = gridDim.x;
+    const long my = nchunks > (long)blockIdx.x ? (nchunks - 1 - blockIdx.x) / G + 1 : 0;
+    const double* rb[2];
+    const double* rh[2];
+    raw_fields<EV>(a, rb, rh);
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int t = 0; t < NR + nctr_maps<EV, EP, K>(); ++t)
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&maps.m[t]) : "memory");
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (long k = 0; k < S - 1 && k < my; ++k) {
+            const long t = blockIdx.x + k * G;
+            issue_chunk<EV, EP, NC, K>(maps, smem + (k % S) * SD, &bars[k % S],
+                                       (int)(t % tiles_c) * 32, (int)(t / tiles_c) * 8, rows,
+                                       ctl.active);
+        }
+    }
+    __syncthreads();
+
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+
+    for (long k = 0; k < my; ++k) {
+        if (threadIdx.x == 0 && k + S - 1 < my) {
+            // refill the stage freed at the end of iteration k-1
+            const long t = blockIdx.x + (k + S - 1) * G;
+            const int ns = (int)((k + S - 1) % S);
+            issue_chunk<EV, EP, NC, K>(maps, smem + ns * SD, &bars[ns], (int)(t % tiles_c) * 32,
+                                       (int)(t / tiles_c) * 8, rows, ctl.active);
+        }
+        const int s = (int)(k % S);
+        const long t = blockIdx.x + k * G;
+        const int j0 = (int)(t % tiles_c) * 32, r0 = (int)(t / tiles_c) * 8;
+        const int i = r0 + wid, j = j0 + lane;
+        mbar_wait(&bars[s], (uint32_t)((k / S) & 1));
+        if (i < rows && j < cols) {
+            const double* raw = smem + s * SD;
+            const double* ctr = raw + NR * NC * RAW_SLOT;
+            const bool gx_m = i == 0, gx_p = i == rows - 1;   // ghost rows (warp-uniform)
+            const bool gy_m = j == 0, gy_p = j == cols - 1;   // ghost columns
+            Nb nb[NC][NCH];
+            double yc[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                double rc[NR], rxm[NR], rxp[NR], rym[NR], ryp[NR];
+#pragma unroll
+                for (int f = 0; f < NR; ++f) {
+                    const double* bx = raw + (f * NC + c) * RAW_SLOT + (1 + wid) * TBW + 2 + lane;
+                    rc[f] = bx[0];
+                    rxm[f] = gx_m ? __ldg(slab_row(a, rb[f], rh[f], c, -1, cols) + j) : bx[-TBW];
+                    rxp[f] = gx_p ? __ldg(slab_row(a, rb[f], rh[f], c, rows, cols) + j) : bx[TBW];
+                    const double* rowg = rb[f] + c * a.npts + (long)i * cols;
+                    rym[f] = gy_m ? __ldg(rowg + wrap_idx(-1, cols, a.g.bc)) : bx[-1];
+                    ryp[f] = gy_p ? __ldg(rowg + wrap_idx(cols, cols, a.g.bc)) : bx[1];
+                }
+                yc[c] = rc[yraw<EV>() < NR ? yraw<EV>() : 0];
+                double hc[NCH], hxm[NCH], hxp[NCH], hym[NCH], hyp[NCH];
+                make_ch<EV, NCH, NR>(ctl, rc, hc);
+                make_ch<EV, NCH, NR>(ctl, rxm, hxm);
+                make_ch<EV, NCH, NR>(ctl, rxp, hxp);
+                make_ch<EV, NCH, NR>(ctl, rym, hym);
+                make_ch<EV, NCH, NR>(ctl, ryp, hyp);
+#pragma unroll
+                for (int h = 0; h < NCH; ++h)
+                    nb[c][h] = Nb{hc[h], hxm[h], hxp[h], hym[h], hyp[h], 0.0, 0.0};
+            }
+            Centre<EV, EP, NC, K> z;
+            const int co = wid * 32 + lane;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                z.fu[c] = FU ? ctr[c * CTR_SLOT + co] : 0.0;
+                if constexpr (EP == EP_LEJA) {
+                    z.y[c] = yc[c];
+#pragma unroll
+                    for (int q = 0; q < K; ++q)
+                        z.p[q][c] = ctr[((FU + q) * NC + c) * CTR_SLOT + co];
+                }
+            }
+            double val[NC];
+            evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
+            epilogue<EV, EP, NC, K>(a, ctl, (long)i * cols + j, val, z, acc);
+        }
+        __syncthreads();  // every warp is done with stage s before it is refilled
+    }
+    reduce_and_finalize<EV, EP, NQ>(a, acc);
+}
+
+}  // namespace ek

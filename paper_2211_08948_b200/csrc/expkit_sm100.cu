@@ -9,8 +9,11 @@
 #include <atomic>
 #include <type_traits>
 
+#include <cudaTypedefs.h>
+
 #include "ek_common.cuh"
 #include "ek_stencil.cuh"
+#include "ek_stream.cuh"
 #include "ek_vector.cuh"
 
 namespace ek {
@@ -181,10 +184,128 @@ static unsigned persistent_grid(Kern kern, int64_t tiles, int& occ_cache) {
     return (unsigned)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
 }
 
+static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// The TMA-staged kernel needs 16-byte aligned row segments of every field.
+static bool tma_ok(const KArgs& a) {
+    if (a.g.dim != 2 || (a.g.n & 1) || a.g.n < 2 || (a.npts & 1)) return false;
+    const void* ps[] = {a.u, a.y, a.k, a.fu, a.hu, a.hy, a.hk};
+    for (const void* p : ps)
+        if (p && !al16(p)) return false;
+    for (int q = 0; q < 8; ++q)
+        if (a.p[q] && !al16(a.p[q])) return false;
+    return true;
+}
+
+static bool g_tma_enabled = true;  // ek_set_tma(0) forces the register-staged kernel
+
+// TMA stage count: as deep as fits two resident blocks per SM.
+template <int EV, int EP, int NC, int K>
+constexpr int tma_stages() {
+    constexpr int bytes = stage_doubles<EV, EP, NC, K>() * 8;
+    return bytes * 4 <= 110 * 1024 ? 4 : (bytes * 3 <= 110 * 1024 ? 3 : 2);
+}
+
+// ---- tensor maps (driver entry point through the runtime, cached)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+struct MapEntry {
+    const void* p;
+    int64_t cols, rows;
+    uint32_t bw, bh;
+    CUtensorMap map;
+};
+
+// (ptr, cols, rows, box) -> encoded map; the Leja / Arnoldi loops reuse a
+// handful of buffers, so the cache turns encoding into a lookup.
+static bool tensor_map(CUtensorMap* out, const double* p, int64_t cols, int64_t rows, uint32_t bw,
+                       uint32_t bh) {
+    static MapEntry cache[64];
+    static int next = 0;
+    for (auto& e : cache)
+        if (e.p == p && e.cols == cols && e.rows == rows && e.bw == bw && e.bh == bh) {
+            *out = e.map;
+            return true;
+        }
+    auto fn = encode_fn();
+    if (!fn) return false;
+    MapEntry& e = cache[next];
+    next = (next + 1) % 64;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * 8};
+    const cuuint32_t box[2] = {bw, bh};
+    const cuuint32_t es[2] = {1, 1};
+    if (fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)p, dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        e.p = nullptr;
+        return false;
+    }
+    e.p = p;
+    e.cols = cols;
+    e.rows = rows;
+    e.bw = bw;
+    e.bh = bh;
+    *out = e.map;
+    return true;
+}
+
+template <int EV, int EP, int NC, int K>
+static bool build_maps(const KArgs& a, TmaMaps& m) {
+    memset(&m, 0, sizeof(m));
+    const int64_t cols = a.g.n, rt = (int64_t)a.g.ncomp * a.g.rows;
+    const double* raw[2] = {nullptr, nullptr};
+    if constexpr (EV == EV_RHS) { raw[0] = a.u; }
+    else if constexpr (EV == EV_LIN) { raw[0] = a.y; }
+    else if constexpr (EV == EV_FD || EV == EV_BURGJ) { raw[0] = a.u; raw[1] = a.y; }
+    else { raw[0] = a.k; raw[1] = a.u; }
+    int t = 0;
+    for (int f = 0; f < nraw<EV>(); ++f)
+        if (!tensor_map(&m.m[t++], raw[f], cols, rt, TBW, TBR)) return false;
+    if constexpr (needs_fu<EV>())
+        if (!tensor_map(&m.m[t++], a.fu, cols, rt, 32, 8)) return false;
+    if constexpr (EP == EP_LEJA)
+        for (int q = 0; q < K && q < a.nk; ++q)
+            if (!tensor_map(&m.m[t++], a.p[q], cols, rt, 32, 8)) return false;
+    return true;
+}
+
 template <class P, int EV, int EP, int K>
 static int launch_k(const KArgs& a, cudaStream_t s) {
     constexpr int RPT = rpt_for(P::NC, ev_nch(EV), P::DIM);
     static int occ = 0;  // one per template instantiation
+    if constexpr (P::DIM == 2) {
+        TmaMaps maps;
+        if (g_tma_enabled && tma_ok(a) && build_maps<EV, EP, P::NC, K>(a, maps)) {
+            constexpr int S = tma_stages<EV, EP, P::NC, K>();
+            constexpr int SMEM = S * stage_doubles<EV, EP, P::NC, K>() * 8;
+            static int tocc = 0;
+            auto kern = k_tma2d<P, EV, EP, K, S>;
+            if (tocc == 0) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, TPB, SMEM) !=
+                        cudaSuccess || tocc < 1)
+                    tocc = 1;
+            }
+            const int64_t chunks = ((a.g.n + 31) / 32) * ((a.g.rows + 7) / 8);
+            const int64_t cap = (int64_t)sm_count() * tocc;
+            const unsigned grid = (unsigned)(chunks < cap ? chunks : cap);
+            kern<<<grid, TPB, SMEM, s>>>(a, maps);
+            EK_LAUNCH_CHECK("tma stencil launch");
+            return EK_OK;
+        }
+    }
     const int64_t tiles = stencil_tiles(&a.g, RPT);
     if constexpr (P::DIM == 3) {
         auto kern = k_stencil3d<P, EV, EP, RPT, K>;
@@ -300,6 +421,11 @@ extern "C" {
 const char* ek_last_error(void) { return g_err; }
 int ek_version(void) { return 1; }
 long long ek_launch_count(void) { return g_launches.load(); }
+int ek_set_tma(int enabled) {
+    const int old = g_tma_enabled ? 1 : 0;
+    g_tma_enabled = enabled != 0;
+    return old;
+}
 
 int ek_copy(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
     const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice

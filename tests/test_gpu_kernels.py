@@ -107,6 +107,49 @@ def test_fused_leja_is_deterministic_and_matches_generic_path():
         assert np.linalg.norm(a - c) <= 1e-7 * np.linalg.norm(c)
 
 
+@pytest.mark.parametrize("mk", [lambda: ext.brusselator_periodic_problem(n=130),
+                                lambda: ek.make_problem("adr", n=66),
+                                lambda: ext.burgers2d_problem(n=96),
+                                lambda: ek.make_problem("gray_scott", n=64)])
+def test_tma_and_register_kernels_agree(mk):
+    """The TMA-staged 2-D kernel and the register-staged one agree bit for
+    bit on every elementwise pass (RHS, FD/analytic Jv, remainder). Passes
+    with a reduction (Leja, power iteration) partition the grid differently,
+    so their norms differ in the last bit and the FD quotient amplifies that:
+    identical counts, vectors within the FD tier."""
+    p = mk()
+    xi = ek.get_leja_points(400)
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal(p.u0.shape)
+    k = p.u0 + 1e-3 * rng.standard_normal(p.u0.shape)
+
+    def run():
+        rhs = ek.CountingRhs(p.rhs)
+        sys_ = ek.make_linearized(rhs, p.u0, jac_factory=p.jac_factory)
+        jv = sys_.J.apply(v)
+        rem = ek.remainder(sys_, k)
+        lam, _ = ek.power_iterate(sys_.J)
+        est = ek.make_estimate(lam)
+        dt = 20.0 / abs(est.alpha)
+        r = ek.leja_interpolate_vertical(sys_.J, sys_.f_n * dt, 1, [0.5, 1.0], dt, est,
+                                         1e-10, xi=xi)
+        return [sys_.f_n, jv, rem], lam, r
+
+    old = N.lib().ek_set_tma(1)
+    try:
+        a, la, ra = run()
+        N.lib().ek_set_tma(0)
+        b, lb, rb = run()
+    finally:
+        N.lib().ek_set_tma(old)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert abs(la - lb) <= 1e-12 * abs(lb)
+    assert ra.iters == rb.iters and ra.freeze_iters == rb.freeze_iters
+    for x, y in zip(ra.vectors, rb.vectors):
+        assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y)
+
+
 def test_leja_fd_charges_match_iterations():
     p = ext.allen_cahn_periodic_problem(n=64)
     rhs = ek.CountingRhs(p.rhs)

@@ -23,11 +23,14 @@ def main():
     ap.add_argument("--k", type=int, default=1)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--problem", default="brusselator_periodic")
+    ap.add_argument("--no-tma", action="store_true")
     args = ap.parse_args()
 
     import torch
     import paper_2211_08948_b200 as ek
-    from paper_2211_08948_b200 import ext, leja as L
+    from paper_2211_08948_b200 import ext, leja as L, _native as NAT
+    if args.no_tma:
+        NAT.lib().ek_set_tma(0)
 
     prob = ext.make_ext_problem(args.problem, n=args.n)
     rhs = ek.CountingRhs(prob.rhs)
