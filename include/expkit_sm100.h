@@ -265,6 +265,18 @@ int ek_vexpr(int64_t len, const int32_t* prog, int nprog,
              const double* scal, int nscal, const double* const* in, int nin,
              double* const* out, int nout, ek_scalar_state* st, double* work,
              void* stream);
+/* Fused linear combinations (the stage algebra's fast path): output o is
+ * fin_o(((t_0 + t_1) + t_2) + ...) with t = in[src] (mode 0), coef*in[src]
+ * (mode 1) or in[src]/coef (mode 2); fin: 0 none, 1 multiply by fval,
+ * 2 divide by fval. src / mode / coef are nout x 6 row-major. out[o] may be
+ * NULL (not stored). rmode 1 reduces output 0, rmode 2 the difference
+ * out0 - out1 (err = ||u5 - u4||): st->val[0] = ||.||^2, val[1] = ||.||,
+ * flag bit0 any nonzero, bit1 any non-finite. */
+int ek_lincomb(int64_t len, const double* const* in, int nin,
+               double* const* out, int nout, const int32_t* nterm,
+               const int32_t* src, const int32_t* mode, const double* coef,
+               const int32_t* fin, const double* fval, int rmode,
+               ek_scalar_state* st, double* work, void* stream);
 /* ||x||^2 -> st->val[slot], ||x|| -> st->val[slot+1]; st->flag bit0 any
  * nonzero, bit1 any non-finite. */
 int ek_norm2(int64_t len, const double* x, ek_scalar_state* st, int slot,

@@ -213,12 +213,132 @@ class _Prog:
             self.emit(_OPC[e.op])
 
 
-def evaluate(outputs, length, norm=False, check=False):
+LT_X, LT_MUL, LT_DIV = 0, 1, 2
+LC_IN, LC_OUT, LC_TERMS = 8, 3, 6
+
+
+def _term(e):
+    """(tensor, mode, coef) for x, c*x, x*c, x/c, -x, -(c*x); else None."""
+    if e.op == "vec":
+        return (e.a, LT_X, 1.0)
+    if e.op == "mul":
+        if e.a.op == "const" and e.b.op == "vec":
+            return (e.b.a, LT_MUL, e.a.a)
+        if e.b.op == "const" and e.a.op == "vec":
+            return (e.a.a, LT_MUL, e.b.a)
+    if e.op == "div" and e.a.op == "vec" and e.b.op == "const":
+        return (e.a.a, LT_DIV, e.b.a)
+    if e.op == "neg":
+        t = _term(e.a)
+        if t is not None:
+            return _negate(t)
+    return None
+
+
+def _negate(t):
+    # a - x == a + (-1)*x, a - c*x == a + (-c)*x, a - x/c == a + x/(-c):
+    # each is bit-identical in IEEE arithmetic (negation is exact)
+    v, m, c = t
+    if m == LT_X:
+        return (v, LT_MUL, -1.0)
+    return (v, m, -c)
+
+
+def _chain(e):
+    """Left-deep +/- chain of terms -> list of terms, else None."""
+    t = _term(e)
+    if t is not None:
+        return [t]
+    if e.op in ("add", "sub"):
+        left = _chain(e.a)
+        right = _term(e.b)
+        if left is None or right is None:
+            return None
+        return left + [right if e.op == "add" else _negate(right)]
+    return None
+
+
+def _fold(e):
+    """(terms, fin_mode, fin_value) for fin(chain) or None."""
+    terms = _chain(e)
+    if terms is not None:
+        return terms, 0, 0.0
+    if e.op == "mul":
+        if e.b.op == "const":
+            inner = _chain(e.a)
+            if inner is not None:
+                return inner, 1, e.b.a
+        if e.a.op == "const":
+            inner = _chain(e.b)
+            if inner is not None:
+                return inner, 1, e.a.a
+    if e.op == "div" and e.b.op == "const":
+        inner = _chain(e.a)
+        if inner is not None:
+            return inner, 2, e.b.a
+    return None
+
+
+def _lincomb(outputs, length, rmode):
+    """Lower to one ek_lincomb launch; False when the expressions do not fit."""
+    folds = [_fold(Expr.wrap(ex)) for ex, _ in outputs]
+    if len(outputs) > LC_OUT or any(f is None or len(f[0]) > LC_TERMS for f in folds):
+        return False
+    ins = []
+
+    def idx(t):
+        for i, x in enumerate(ins):
+            if x.data_ptr() == t.data_ptr() and x.numel() == t.numel():
+                return i
+        ins.append(t)
+        return len(ins) - 1
+
+    nout = len(outputs)
+    nterm = (C.c_int32 * nout)()
+    src = (C.c_int32 * (nout * LC_TERMS))()
+    mode = (C.c_int32 * (nout * LC_TERMS))()
+    coef = (C.c_double * (nout * LC_TERMS))()
+    fin = (C.c_int32 * nout)()
+    fval = (C.c_double * nout)()
+    for o, (terms, fm, fv) in enumerate(folds):
+        nterm[o] = len(terms)
+        for t, (v, m, c) in enumerate(terms):
+            src[o * LC_TERMS + t] = idx(v)
+            mode[o * LC_TERMS + t] = m
+            coef[o * LC_TERMS + t] = float(c)
+        fin[o] = fm
+        fval[o] = float(fv)
+    if len(ins) > LC_IN:
+        return False
+    return ins, nterm, src, mode, coef, fin, fval
+
+
+def evaluate(outputs, length, norm=False, check=False, norm_diff=False):
     """Run one fused elementwise pass.
 
     outputs: list of (Expr, out_tensor_or_None). norm/check apply to the
-    first expression: returns (||value||, flags) after a sync when either
-    is requested, else None."""
+    first expression (norm_diff: to the difference of the first two):
+    returns (||value||, flags) after a sync when requested, else None.
+    Linear combinations go to `ek_lincomb`; anything else to the general
+    elementwise program `ek_vexpr`."""
+    rmode = 2 if norm_diff else (1 if (norm or check) else 0)
+    low = _lincomb(outputs, length, rmode)
+    if low:
+        ins, nterm, src, mode, coef, fin, fval = low
+        outs = [o for _, o in outputs]
+        st = scalar_state() if rmode else None
+        N.check(N.lib().ek_lincomb(
+            int(length), N.ptrs(ins), len(ins), N.ptrs(outs), len(outs), nterm, src, mode,
+            coef, fin, fval, rmode, st.ptr if st else None, work_ptr() if st else None,
+            stream()), "ek_lincomb")
+        if st is None:
+            return None
+        h = st.read()
+        return float(h.val[1]), int(h.flag)
+    if norm_diff:
+        a, b = outputs[0][0], outputs[1][0]
+        evaluate(outputs, length)
+        return evaluate([(Expr.wrap(a) - Expr.wrap(b), None)], length, norm=True)
     pr = _Prog()
     outs = []
     for i, (ex, out) in enumerate(outputs):

@@ -102,6 +102,9 @@ _SIGS = {
     "ek_norm2": (_I, [_L, _P, _P, _I, _P, _P]),
     "ek_l1": (_I, [_L, _P, _P, _I, _P, _P]),
     "ek_selftest_div": (_I, [_L, _P, _P, _P, _P, _P]),
+    "ek_lincomb": (_I, [_L, _PP, _I, _PP, _I, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                        C.POINTER(C.c_int32), C.POINTER(_D), C.POINTER(C.c_int32),
+                        C.POINTER(_D), _I, _P, _P, _P]),
     "ek_dense_gemv": (_I, [_L, _P, _P, _P, _P]),
 }
 

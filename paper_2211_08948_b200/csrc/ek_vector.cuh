@@ -461,6 +461,101 @@ __global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
     }
 }
 
+// ------------------------------------------------------------- lincomb
+// Up to LC_OUT outputs, each a left fold over up to LC_TERMS terms of up to
+// LC_IN shared inputs: out = fin(((t0 + t1) + t2) + ...), term = x, c*x or
+// x/c, fin = identity, *s or /s. This covers every stage expression of the
+// steppers in NumPy's exact rounding order (a - c*b is folded as
+// a + (-c)*b, which is bit-identical). Output 0 may be "virtual" (not
+// stored) and is the one reduced: ||out0||^2 and nonzero / non-finite flags.
+constexpr int LC_IN = 8, LC_OUT = 3, LC_TERMS = 6;
+enum { LT_X = 0, LT_MUL = 1, LT_DIV = 2 };
+struct LincombArgs {
+    int64_t len;
+    const double* in[LC_IN];
+    double* out[LC_OUT];
+    int nout;
+    int nterm[LC_OUT];
+    int src[LC_OUT][LC_TERMS];
+    int mode[LC_OUT][LC_TERMS];
+    Dv coef[LC_OUT][LC_TERMS];   // c (LT_MUL: c.d is the factor) or divisor
+    int fin[LC_OUT];             // 0 none, 1 multiply, 2 divide
+    Dv fval[LC_OUT];
+    int reduce;
+    ek_scalar_state* st;
+    double* work;
+};
+
+__device__ __forceinline__ double lc_term(const LincombArgs& a, int o, int t, double x) {
+    const int m = a.mode[o][t];
+    if (m == LT_MUL) return a.coef[o][t].d * x;
+    if (m == LT_DIV) return dv(x, a.coef[o][t]);
+    return x;
+}
+
+template <int NOUT>
+__global__ void __launch_bounds__(TPB) k_lincomb(const LincombArgs a) {
+    double acc[1] = {0.0};
+    double red[3] = {0.0, 0.0, 0.0};
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
+         e += (int64_t)gridDim.x * TPB) {
+        double xin[LC_IN];
+#pragma unroll
+        for (int i = 0; i < LC_IN; ++i) xin[i] = 0.0;
+        // load each input once (the compiler hoists these independent loads)
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+            for (int t = 0; t < LC_TERMS; ++t)
+                if (t < a.nterm[o]) {
+#pragma unroll
+                    for (int i = 0; i < LC_IN; ++i)
+                        if (a.src[o][t] == i && a.in[i]) xin[i] = __ldg(a.in[i] + e);
+                }
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+            const int nt = a.nterm[o];
+            double s = 0.0;
+#pragma unroll
+            for (int t = 0; t < LC_TERMS; ++t) {
+                if (t < nt) {
+                    double x = 0.0;
+#pragma unroll
+                    for (int i = 0; i < LC_IN; ++i)
+                        if (a.src[o][t] == i) x = xin[i];
+                    const double v = lc_term(a, o, t, x);
+                    s = t == 0 ? v : s + v;
+                }
+            }
+            if (a.fin[o] == 1) s = s * a.fval[o].d;
+            else if (a.fin[o] == 2) s = dv(s, a.fval[o]);
+            if (a.out[o]) a.out[o][e] = s;
+            if (o == 0) {
+                acc[0] = s;  // kept for the reduction below
+            } else if (o == 1 && a.reduce == 2) {
+                acc[0] = acc[0] - s;  // ||out0 - out1||
+            }
+        }
+        const double r = acc[0];
+        acc[0] = 0.0;
+        red[0] += r * r;
+        red[1] += r != 0.0 ? 1.0 : 0.0;
+        red[2] += isfinite(r) ? 0.0 : 1.0;
+    }
+    if (a.reduce) {
+        block_sum<3>(red);
+        if (publish_and_arrive<3>(red, a.work, &a.st->ticket)) {
+            double tot[3];
+            gather_partials<3>(a.work, gridDim.x, tot);
+            if (threadIdx.x == 0) {
+                a.st->val[0] = tot[0];
+                a.st->val[1] = sqrt(tot[0]);
+                a.st->flag |= (tot[1] > 0.0 ? 1 : 0) | (tot[2] > 0.0 ? 2 : 0);
+            }
+        }
+    }
+}
+
 // --------------------------------------------------------- self test
 // fast[i] = dv(x[i], mkdv(d[i])), exact[i] = x[i] / d[i] (division
 // instruction): proves the reciprocal-correction quotient is bit-identical.

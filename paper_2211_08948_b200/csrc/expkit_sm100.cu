@@ -792,6 +792,56 @@ int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot, double* w
     return EK_OK;
 }
 
+int ek_lincomb(int64_t len, const double* const* in, int nin, double* const* out, int nout,
+               const int32_t* nterm, const int32_t* src, const int32_t* mode, const double* coef,
+               const int32_t* fin, const double* fval, int rmode, ek_scalar_state* st,
+               double* work, void* stream) {
+    if (nin < 1 || nin > LC_IN || nout < 1 || nout > LC_OUT) {
+        set_error("ek_lincomb: nin=%d nout=%d out of range", nin, nout);
+        return EK_ERR_INVALID;
+    }
+    LincombArgs a;
+    memset(&a, 0, sizeof(a));
+    a.len = len;
+    a.nout = nout;
+    for (int i = 0; i < nin; ++i) a.in[i] = in[i];
+    for (int o = 0; o < nout; ++o) {
+        a.out[o] = out[o];
+        a.nterm[o] = nterm[o];
+        if (nterm[o] < 1 || nterm[o] > LC_TERMS) {
+            set_error("ek_lincomb: %d terms", nterm[o]);
+            return EK_ERR_INVALID;
+        }
+        for (int t = 0; t < nterm[o]; ++t) {
+            const int k = o * LC_TERMS + t;
+            if (src[k] < 0 || src[k] >= nin) {
+                set_error("ek_lincomb: bad source %d", src[k]);
+                return EK_ERR_INVALID;
+            }
+            a.src[o][t] = src[k];
+            a.mode[o][t] = mode[k];
+            a.coef[o][t] = mode[k] == LT_DIV ? mkdv(coef[k]) : Dv{coef[k], 0.0};
+        }
+        a.fin[o] = fin[o];
+        a.fval[o] = fin[o] == 2 ? mkdv(fval[o]) : Dv{fval[o], 0.0};
+    }
+    if (rmode && (!st || !work || (rmode == 2 && nout < 2))) {
+        set_error("ek_lincomb: reduction mode %d needs a state block, workspace (and 2 outputs)",
+                  rmode);
+        return EK_ERR_INVALID;
+    }
+    a.reduce = rmode;
+    a.st = st;
+    a.work = work;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = vgrid(len);
+    if (nout == 1) k_lincomb<1><<<g, TPB, 0, s>>>(a);
+    else if (nout == 2) k_lincomb<2><<<g, TPB, 0, s>>>(a);
+    else k_lincomb<3><<<g, TPB, 0, s>>>(a);
+    EK_LAUNCH_CHECK("k_lincomb");
+    return EK_OK;
+}
+
 int ek_selftest_div(int64_t n, const double* x, const double* d, double* fast, double* exact,
                     void* stream) {
     k_selftest_div<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(n, x, d, fast, exact);

@@ -35,6 +35,46 @@ def test_reciprocal_division_is_bit_exact():
     assert np.array_equal(f, e), int(np.sum(f != e))
 
 
+def test_stage_algebra_bit_exact_vs_numpy():
+    """Every stage-expression shape of integrators.py, lowered to the fused
+    lincomb kernel (or the general program), equals NumPy bit for bit."""
+    rng = np.random.default_rng(11)
+    n = 100_003
+    a, b, c, d = (rng.standard_normal(n) * 10.0 ** rng.uniform(-5, 5, n) for _ in range(4))
+    A, B, Cc, Dd = (D.to_dev(x) for x in (a, b, c, d))
+    X = D.V
+    dt = 3.3e-5
+    cases = [
+        (X(A) + (1.0 / 8.0) * X(B), a + (1.0 / 8.0) * b),
+        ((-1024.0 * X(A) + 1458.0 * X(B)) * dt, (-1024.0 * a + 1458.0 * b) * dt),
+        (X(A) + 0.84405472011657126298 * X(B) + 1.6905891609568963624 * X(Cc),
+         a + 0.84405472011657126298 * b + 1.6905891609568963624 * c),
+        ((-2.0 * X(A) + X(B)) * dt, (-2.0 * a + b) * dt),
+        (X(A) + 0.9 * X(B) + (27.0 / 25.0) * X(Cc) + (729.0 / 125.0) * X(Dd),
+         a + 0.9 * b + (27.0 / 25.0) * c + (729.0 / 125.0) * d),
+        ((16.0 * X(A) - 2.0 * X(B)) * dt, (16.0 * a - 2.0 * b) * dt),
+        (X(A) + X(B) + X(Cc) + X(Dd), a + b + c + d),
+        (X(A) / (0.5 ** 3), a / (0.5 ** 3)),
+        ((X(A) - X(B)) / 1.7e-9, (a - b) / 1.7e-9),
+        ((X(A) - X(B)) - X(Cc), (a - b) - c),
+        (X(A) * dt, a * dt),
+        (X(A) + X(B) * dt, a + b * dt),
+        (1.0 - X(A) * X(B), 1.0 - a * b),           # general program path
+    ]
+    for ex, ref in cases:
+        got = D.ev(ex, n).cpu().numpy()
+        assert np.array_equal(got, ref)
+    # fused multi-output + ||out0 - out1||
+    u5, u4 = D.empty(n), D.empty(n)
+    common = X(A) + 1.0 * X(B)
+    err, _ = D.evaluate([(common + 2.5 * X(Cc), u5), (common + 0.5 * X(Dd), u4)], n,
+                        norm_diff=True)
+    r5 = a + 1.0 * b + 2.5 * c
+    r4 = a + 1.0 * b + 0.5 * d
+    assert np.array_equal(u5.cpu().numpy(), r5) and np.array_equal(u4.cpu().numpy(), r4)
+    assert err == pytest.approx(np.linalg.norm(r5 - r4), rel=1e-13)
+
+
 RAGGED = [
     ("adr", lambda n: ek.make_problem("adr", alpha=0.1, n=n), lambda n: OF.make("adr", alpha=0.1, n=n)),
     ("bruss", lambda n: ek.make_problem("brusselator", n=n), lambda n: OF.make("brusselator", n=n)),
