@@ -292,15 +292,13 @@ def e2e(args, ek, prob, dt, xi):
 
     def step(u):
         nonlocal jv
-        sys_ = ek.make_linearized(rhs, u)
+        sys_ = ek.make_linearized(rhs, u)        # NumPy state in: host -> device
         c1 = rhs.counter.count
         ctx.est = ek.maybe_refresh(ctx.est, sys_.J, policy)
         c2 = rhs.counter.count
         res = ek.take_step(INTEGRATOR, sys_, dt, "leja", TOL, ctx)
         jv += res.stats.leja_iters + (c2 - c1) + res.stats.group_rhs_evals.get("remainder", 0) // 2
-        out = res.u_high  # NumPy: device -> host
-        u_host[:] = out
-        return u_host
+        return res.u_high                         # NumPy state out: device -> host
 
     u = u_host
     for _ in range(min(args.warmup, 2)):

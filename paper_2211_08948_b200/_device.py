@@ -47,15 +47,27 @@ def to_dev(x, copy=False):
     return torch.from_numpy(arr).to(device=device())
 
 
+_PIN_MIN = 1 << 20  # bytes; larger results come back through pinned memory
+
+
 def like_input(t, ref):
     """Return t in the kind of `ref`: numpy in -> numpy out, tensor -> tensor."""
     if isinstance(ref, torch.Tensor):
         return t
-    return t.cpu().numpy()
+    return to_host(t)
 
 
 def to_host(t):
-    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+    """Device -> NumPy. Large vectors are copied into page-locked memory
+    (torch's caching host allocator), a direct DMA at full PCIe rate; the
+    array keeps its pinned buffer alive and a later H2D of it is direct too."""
+    if not isinstance(t, torch.Tensor):
+        return np.asarray(t)
+    if t.is_cuda and t.numel() * t.element_size() >= _PIN_MIN:
+        host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        host.copy_(t)
+        return host.numpy()
+    return t.cpu().numpy()
 
 
 def empty(n):
