@@ -493,54 +493,78 @@ __device__ __forceinline__ double lc_term(const LincombArgs& a, int o, int t, do
     return x;
 }
 
-template <int NOUT>
+// 4 consecutive elements per thread and iteration (two 16-byte loads per
+// term), all term loads issued before the fold.
+template <int NOUT, bool ALIGNED>
 __global__ void __launch_bounds__(TPB) k_lincomb(const LincombArgs a) {
-    double acc[1] = {0.0};
+    constexpr int W = 4;
     double red[3] = {0.0, 0.0, 0.0};
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
-         e += (int64_t)gridDim.x * TPB) {
-        double xin[LC_IN];
-#pragma unroll
-        for (int i = 0; i < LC_IN; ++i) xin[i] = 0.0;
-        // load each input once (the compiler hoists these independent loads)
-#pragma unroll
-        for (int o = 0; o < NOUT; ++o)
-#pragma unroll
-            for (int t = 0; t < LC_TERMS; ++t)
-                if (t < a.nterm[o]) {
-#pragma unroll
-                    for (int i = 0; i < LC_IN; ++i)
-                        if (a.src[o][t] == i && a.in[i]) xin[i] = __ldg(a.in[i] + e);
-                }
+    const int64_t ngroups = (a.len + W - 1) / W;
+    for (int64_t gi = (int64_t)blockIdx.x * TPB + threadIdx.x; gi < ngroups;
+         gi += (int64_t)gridDim.x * TPB) {
+        const int64_t e0 = gi * W;
+        const bool full = ALIGNED && e0 + W <= a.len;
+        double r[W];
 #pragma unroll
         for (int o = 0; o < NOUT; ++o) {
-            const int nt = a.nterm[o];
-            double s = 0.0;
+            double x[LC_TERMS][W];
 #pragma unroll
             for (int t = 0; t < LC_TERMS; ++t) {
-                if (t < nt) {
-                    double x = 0.0;
+                if (t < a.nterm[o]) {
+                    const double* p = a.in[a.src[o][t]] + e0;
+                    if (full) {
+                        const double2 v0 = __ldg(reinterpret_cast<const double2*>(p));
+                        const double2 v1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
+                        x[t][0] = v0.x; x[t][1] = v0.y; x[t][2] = v1.x; x[t][3] = v1.y;
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < LC_IN; ++i)
-                        if (a.src[o][t] == i) x = xin[i];
-                    const double v = lc_term(a, o, t, x);
-                    s = t == 0 ? v : s + v;
+                        for (int w = 0; w < W; ++w) x[t][w] = e0 + w < a.len ? __ldg(p + w) : 0.0;
+                    }
                 }
             }
-            if (a.fin[o] == 1) s = s * a.fval[o].d;
-            else if (a.fin[o] == 2) s = dv(s, a.fval[o]);
-            if (a.out[o]) a.out[o][e] = s;
-            if (o == 0) {
-                acc[0] = s;  // kept for the reduction below
-            } else if (o == 1 && a.reduce == 2) {
-                acc[0] = acc[0] - s;  // ||out0 - out1||
+            double s[W];
+#pragma unroll
+            for (int t = 0; t < LC_TERMS; ++t) {
+                if (t < a.nterm[o]) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        const double v = lc_term(a, o, t, x[t][w]);
+                        s[w] = t == 0 ? v : s[w] + v;
+                    }
+                }
+            }
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                if (a.fin[o] == 1) s[w] = s[w] * a.fval[o].d;
+                else if (a.fin[o] == 2) s[w] = dv(s[w], a.fval[o]);
+            }
+            double* q = a.out[o];
+            if (q) {
+                if (full) {
+                    reinterpret_cast<double2*>(q + e0)[0] = make_double2(s[0], s[1]);
+                    reinterpret_cast<double2*>(q + e0)[1] = make_double2(s[2], s[3]);
+                } else {
+#pragma unroll
+                    for (int w = 0; w < W; ++w)
+                        if (e0 + w < a.len) q[e0 + w] = s[w];
+                }
+            }
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                if (o == 0) r[w] = s[w];
+                else if (o == 1 && a.reduce == 2) r[w] = r[w] - s[w];  // ||out0 - out1||
             }
         }
-        const double r = acc[0];
-        acc[0] = 0.0;
-        red[0] += r * r;
-        red[1] += r != 0.0 ? 1.0 : 0.0;
-        red[2] += isfinite(r) ? 0.0 : 1.0;
+        if (a.reduce) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                if (e0 + w < a.len) {
+                    red[0] += r[w] * r[w];
+                    red[1] += r[w] != 0.0 ? 1.0 : 0.0;
+                    red[2] += isfinite(r[w]) ? 0.0 : 1.0;
+                }
+            }
+        }
     }
     if (a.reduce) {
         block_sum<3>(red);

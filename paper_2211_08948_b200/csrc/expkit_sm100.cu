@@ -834,10 +834,19 @@ int ek_lincomb(int64_t len, const double* const* in, int nin, double* const* out
     a.st = st;
     a.work = work;
     cudaStream_t s = (cudaStream_t)stream;
-    const int g = vgrid(len);
-    if (nout == 1) k_lincomb<1><<<g, TPB, 0, s>>>(a);
-    else if (nout == 2) k_lincomb<2><<<g, TPB, 0, s>>>(a);
-    else k_lincomb<3><<<g, TPB, 0, s>>>(a);
+    const int g = vgrid((len + 3) / 4);  // 4 elements per thread and iteration
+    bool aligned = true;
+    for (int i = 0; i < nin; ++i) aligned = aligned && al16(in[i]);
+    for (int o = 0; o < nout; ++o) aligned = aligned && (!out[o] || al16(out[o]));
+    if (aligned) {
+        if (nout == 1) k_lincomb<1, true><<<g, TPB, 0, s>>>(a);
+        else if (nout == 2) k_lincomb<2, true><<<g, TPB, 0, s>>>(a);
+        else k_lincomb<3, true><<<g, TPB, 0, s>>>(a);
+    } else {
+        if (nout == 1) k_lincomb<1, false><<<g, TPB, 0, s>>>(a);
+        else if (nout == 2) k_lincomb<2, false><<<g, TPB, 0, s>>>(a);
+        else k_lincomb<3, false><<<g, TPB, 0, s>>>(a);
+    }
     EK_LAUNCH_CHECK("k_lincomb");
     return EK_OK;
 }
