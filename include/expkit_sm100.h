@@ -98,6 +98,11 @@ typedef struct ek_leja_state {
     uint32_t ticket;    /* internal: last-block counter (keep 0)            */
     int32_t iters;      /* iteration count at termination                   */
     int32_t freeze[8];  /* freeze_iters                                     */
+    int32_t defer;      /* slab mode: kernels leave their local sums in
+                           part[] and ek_leja_decide applies the decision
+                           to the rank-ordered global sums                  */
+    int32_t pad_;
+    double part[2];     /* local ||y||^2 and non-finite count                */
 } ek_leja_state;
 
 /* Scalar reduction slot (norms, dots, flags), device memory. */
@@ -124,7 +129,8 @@ typedef struct ek_power_state {
     int32_t fd_evals;
     uint32_t ticket;    /* internal (keep 0)                                */
     int32_t status;     /* EK_ST_*                                          */
-    int32_t pad_;
+    int32_t defer;      /* slab mode, see ek_leja_state                     */
+    double part[2];     /* local sums of the last pass                      */
 } ek_power_state;
 
 /* KIOPS Arnoldi control block (kiops.py:168-194). Host initialises nu, tol. */
@@ -179,7 +185,7 @@ int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu,
  * with the caller's eps from ||k-u||. st->flag bit1: non-finite output. */
 int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu,
                  const double* k, double eps, double* out, ek_scalar_state* st,
-                 double* work, void* stream);
+                 double* work, const double* const* halo, void* stream);
 
 /* ------------------------------------------------------- Leja (leja.py) */
 /* Coefficient table coef_dev: (k+1) rows x 32 columns, row 0 the shifts
@@ -201,7 +207,8 @@ int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
 int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu,
                 const double* b, double* const* ybuf, double* const* p, int k,
                 const double* coef_dev, int chunk_base, int m_begin, int m_end,
-                double gamma, ek_leja_state* st, double* work, void* stream);
+                double gamma, ek_leja_state* st, double* work,
+                const double* const* halo, void* stream);
 
 /* One recurrence step for a Jacobian action computed elsewhere (dense,
  * callable or 1-D operators): y' = jv/gamma - shift*y, accumulators, norm,
@@ -219,7 +226,24 @@ int ek_leja_update(int64_t len, const double* jv, const double* y,
  * identical to the reference's v = w / nw). Output ping-pongs in wbuf. */
 int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu,
                  const double* v0, double* const* wbuf, int it_begin,
-                 int it_end, ek_power_state* st, double* work, void* stream);
+                 int it_end, ek_power_state* st, double* work,
+                 const double* const* halo, void* stream);
+/* ||x||^2 (scaled = 0: divisor of the start vector; 1: ||x/nw|| for the FD
+ * increment) into the power state (part[] in slab mode). */
+int ek_power_norm(int64_t len, const double* x, int scaled, ek_power_state* st,
+                  double* work, void* stream);
+
+/* ----------------------------------------------- slab (multi-GPU) mode */
+/* With state->defer = 1 the reducing kernels leave their local sums in
+ * state->part[2]; the caller all-gathers the part[] pairs of every rank
+ * (`gathered` = nranks x 2 doubles, device) and applies the decision with
+ * the rank-ordered global sums: */
+int ek_leja_decide(ek_leja_state* st, const double* gathered, int nranks,
+                   const double* coef_dev, int chunk_base, int m, int k, int fd,
+                   int begin, void* stream);
+/* which: 0 = power iteration step, 1 = ||v0||, 2 = ||v|| (FD increment). */
+int ek_power_decide(ek_power_state* st, const double* gathered, int nranks,
+                    int fd, int which, void* stream);
 
 /* --------------------------------------------------- KIOPS (kiops.py) */
 /* V[0] = [src ; tail], beta = ||V[0]||, V[0] /= beta, ||V[0,:n]||

@@ -132,21 +132,38 @@ def scalar_state():
     return DevState(N.ScalarState)
 
 
+# Slab communicator of this process (set by slab.distribute): reductions of
+# distributed vectors become rank-ordered global sums. One decomposition
+# per process (one process per GPU).
+COMM = None
+
+
+def global_norm(h):
+    """(||x||, flags) from a reduced ek_scalar_state, global in slab mode."""
+    if COMM is None:
+        return float(h.val[1]), int(h.flag)
+    s, nz, nf = COMM.allsum([float(h.val[0]), float(h.flag & 1), float((h.flag >> 1) & 1)])
+    return math.sqrt(s), (1 if nz > 0 else 0) | (2 if nf > 0 else 0)
+
+
+def global_sum(v):
+    return v if COMM is None else COMM.allsum([float(v)])[0]
+
+
 def norm2(x, st=None):
     """(||x||, flags) of a device vector; synchronises. flags bit0: any
     nonzero, bit1: any non-finite."""
     st = st or scalar_state()
     N.check(N.lib().ek_norm2(x.numel(), C.c_void_p(x.data_ptr()), st.ptr, 0,
                              work_ptr(), stream()), "ek_norm2")
-    h = st.read()
-    return float(h.val[1]), int(h.flag)
+    return global_norm(st.read())
 
 
 def l1(x):
     st = scalar_state()
     N.check(N.lib().ek_l1(x.numel(), C.c_void_p(x.data_ptr()), st.ptr, 0,
                           work_ptr(), stream()), "ek_l1")
-    return float(st.read().val[0])
+    return global_sum(float(st.read().val[0]))
 
 
 # ------------------------------------------------------- vexpr builder
@@ -345,8 +362,7 @@ def evaluate(outputs, length, norm=False, check=False, norm_diff=False):
             stream()), "ek_lincomb")
         if st is None:
             return None
-        h = st.read()
-        return float(h.val[1]), int(h.flag)
+        return global_norm(st.read())
     if norm_diff:
         a, b = outputs[0][0], outputs[1][0]
         evaluate(outputs, length)
@@ -374,8 +390,7 @@ def evaluate(outputs, length, norm=False, check=False, norm_diff=False):
         work_ptr() if st else None, stream()), "ek_vexpr")
     if st is None:
         return None
-    h = st.read()
-    return float(h.val[1]), int(h.flag)
+    return global_norm(st.read())
 
 
 def ev(expr, length=None, out=None):

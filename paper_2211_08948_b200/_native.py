@@ -38,7 +38,8 @@ class LejaState(C.Structure):
                 ("tol", C.c_double), ("m", C.c_int32), ("done", C.c_int32),
                 ("status", C.c_int32), ("k", C.c_int32), ("active", C.c_uint32),
                 ("fd_evals", C.c_int32), ("ticket", C.c_uint32),
-                ("iters", C.c_int32), ("freeze", C.c_int32 * 8)]
+                ("iters", C.c_int32), ("freeze", C.c_int32 * 8), ("defer", C.c_int32),
+                ("pad_", C.c_int32), ("part", C.c_double * 2)]
 
 
 class ScalarState(C.Structure):
@@ -53,7 +54,7 @@ class PowerState(C.Structure):
                 ("max_it", C.c_int32), ("done", C.c_int32),
                 ("converged", C.c_int32), ("fd_evals", C.c_int32),
                 ("ticket", C.c_uint32), ("status", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("defer", C.c_int32), ("part", C.c_double * 2)]
 
 
 class ArnoldiState(C.Structure):
@@ -81,14 +82,17 @@ _SIGS = {
     "ek_sync": (_I, [_P]),
     "ek_rhs": (_I, [C.POINTER(Grid), _P, _P, _PP, _P]),
     "ek_jv": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _P, _P, _PP, _P]),
-    "ek_remainder": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _P, _P, _P]),
+    "ek_remainder": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _P, _P, _PP, _P]),
     "ek_leja_begin_len": (_I, [_L, _P, _PP, _I, _P, _P, _P, _P]),
     "ek_leja_run": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
-                         _I, _I, _D, _P, _P, _P]),
+                         _I, _I, _D, _P, _P, _PP, _P]),
     "ek_leja_update": (_I, [_L, _P, _P, _P, _PP, _I, _P, _I, _I, _D, _I, _P,
                             _P, _P]),
     "ek_power_run": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _I, _I, _P, _P,
-                          _P]),
+                          _PP, _P]),
+    "ek_power_norm": (_I, [_L, _P, _I, _P, _P, _P]),
+    "ek_leja_decide": (_I, [_P, _P, _I, _P, _I, _I, _I, _I, _I, _P]),
+    "ek_power_decide": (_I, [_P, _P, _I, _I, _I, _P]),
     "ek_arnoldi_init": (_I, [_L, _I, _P, C.POINTER(_D), _P, _P, _P, _P]),
     "ek_arnoldi_run": (_I, [C.POINTER(Grid), _I, _P, _P, _PP, _PP,
                             C.POINTER(_I), _I, _D, _I, _I, _P, _P, _I, _I, _I,

@@ -40,6 +40,7 @@
 #pragma once
 
 #include "ek_common.cuh"
+#include "ek_decide.cuh"
 
 namespace ek {
 
@@ -655,62 +656,20 @@ template <int EV, int EP>
 __device__ void finalize(const KArgs& a, const double* tot) {
     if constexpr (EP == EP_LEJA) {
         ek_leja_state* st = (ek_leja_state*)a.st;
-        const int m = a.m;
-        const double ny = sqrt(tot[0]);  // np.linalg.norm(y)   leja.py:173
-        if (EV == EV_FD && st->ny != 0.0) st->fd_evals += 1;
-        if (EV == EV_FD && tot[1] > 0.0) {
-            st->status = EK_ST_JV_NONFINITE;  // linalg.py:127-128
-            st->done = 1;
-            st->iters = m;
+        if (st->defer) {  // slab mode: ek_leja_decide finishes with global sums
+            st->part[0] = tot[0];
+            st->part[1] = tot[1];
             return;
         }
-        if (!isfinite(ny)) {
-            st->status = EK_ST_NORM_NONFINITE;  // leja.py:174-175
-            st->done = 1;
-            st->iters = m;
-            return;
-        }
-        uint32_t act = st->active;
-        for (int q = 0; q < a.nk; ++q) {
-            if ((act >> q) & 1u) {
-                const double dq = a.coef[(1 + q) * 32 + a.mi];
-                if (fabs(dq) * ny < st->tol) {  // leja.py:180
-                    act &= ~(1u << q);
-                    st->freeze[q] = m;
-                }
-            }
-        }
-        st->active = act;
-        st->ny = ny;
-        st->m = m;
-        st->eps = (SQRT_EPS * (1.0 + st->nu)) / ny;  // linalg.py:123
-        if (act == 0u) {
-            st->done = 1;
-            st->iters = m;
-        }
+        leja_decide(st, a.coef, a.mi, a.m, a.nk, tot[0], tot[1], EV == EV_FD);
     } else if constexpr (EP == EP_POWER) {
         ek_power_state* st = (ek_power_state*)a.st;
-        const double nw = sqrt(tot[0]);  // spectrum.py:58
-        if (EV == EV_FD) st->fd_evals += 1;
-        if (EV == EV_FD && tot[1] > 0.0) {
-            st->status = EK_ST_JV_NONFINITE;
-            st->done = 1;
+        if (st->defer) {
+            st->part[0] = tot[0];
+            st->part[1] = tot[1];
             return;
         }
-        st->it += 1;
-        if (nw == 0.0) {  // spectrum.py:59-60
-            st->lam = 0.0;
-            st->converged = 1;
-            st->done = 1;
-        } else if (fabs(nw - st->lam) <= st->tol_pi * nw) {  // spectrum.py:63
-            st->lam = nw;
-            st->converged = 1;
-            st->done = 1;
-        } else {
-            st->lam = nw;
-            if (st->it >= st->max_it) st->done = 1;
-        }
-        st->nw = nw;
+        power_decide(st, tot[0], tot[1], EV == EV_FD);
     } else if constexpr (EP == EP_ARN) {
         ek_arnoldi_state* st = (ek_arnoldi_state*)a.st;
         if (EV == EV_FD && st->nvn != 0.0) st->fd_evals += 1;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "ek_common.cuh"
+#include "ek_decide.cuh"
 
 namespace ek {
 
@@ -93,22 +94,40 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
         double tot[1];
         gather_partials<1>(a.work, gridDim.x, tot);
         if (threadIdx.x == 0) {
-            ek_leja_state* st = a.st;
-            const double ny = sqrt(tot[0]);
-            uint32_t act = 0u;
-            for (int q = 0; q < a.nk; ++q) {
-                if (!(fabs(d[q]) * ny < st->tol)) act |= 1u << q;
-                st->freeze[q] = 0;
+            if (a.st->defer) {
+                a.st->part[0] = tot[0];
+                a.st->part[1] = 0.0;
+            } else {
+                leja_begin_decide(a.st, a.coef, a.nk, tot[0]);
             }
-            st->active = act;
-            st->ny = ny;
-            st->m = 0;
-            st->status = EK_ST_OK;
-            st->eps = (SQRT_EPS * (1.0 + st->nu)) / ny;
-            st->done = act == 0u ? 1 : 0;
-            st->iters = 0;
         }
     }
+}
+
+// Slab mode: apply a deferred Leja decision to the gathered per-rank sums
+// (`g` = [nranks][2] part[] pairs, summed in rank order).
+__global__ void k_leja_decide(ek_leja_state* st, const double* g, int nranks, const double* coef,
+                              int mi, int m, int nk, int fd, int begin) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (!begin && st->done) return;
+    double s0, s1;
+    gathered_sums(g, nranks, s0, s1);
+    if (begin) leja_begin_decide(st, coef, nk, s0);
+    else leja_decide(st, coef, mi, m, nk, s0, s1, fd != 0);
+}
+
+// Slab mode: deferred power-iteration decision; which = 0 iteration,
+// 1 = ||v0|| (first divisor), 2 = ||v|| (FD increment).
+__global__ void k_power_decide(ek_power_state* st, const double* g, int nranks, int fd,
+                               int which) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (which == 0 && (st->done || st->status)) return;
+    if (which == 2 && (st->done || st->status)) return;
+    double s0, s1;
+    gathered_sums(g, nranks, s0, s1);
+    if (which == 0) power_decide(st, s0, s1, fd != 0);
+    else if (which == 1) st->nw = sqrt(s0);
+    else st->nv = sqrt(s0);
 }
 
 // One recurrence step for a Jacobian action computed elsewhere
@@ -137,29 +156,12 @@ __global__ void __launch_bounds__(TPB) k_leja_update(const LejaVArgs a) {
         double tot[1];
         gather_partials<1>(a.work, gridDim.x, tot);
         if (threadIdx.x == 0) {
-            ek_leja_state* st = a.st;
-            const int m = a.m;
-            const double ny = sqrt(tot[0]);
-            if (!isfinite(ny)) {
-                st->status = EK_ST_NORM_NONFINITE;
-                st->done = 1;
-                st->iters = m;
-                return;
-            }
-            uint32_t ac = st->active;
-            for (int q = 0; q < a.nk; ++q) {
-                if (((ac >> q) & 1u) && fabs(d[q]) * ny < st->tol) {
-                    ac &= ~(1u << q);
-                    st->freeze[q] = m;
-                }
-            }
-            st->active = ac;
-            st->ny = ny;
-            st->m = m;
-            st->eps = (SQRT_EPS * (1.0 + st->nu)) / ny;
-            if (ac == 0u) {
-                st->done = 1;
-                st->iters = m;
+            if (a.st->defer) {
+                a.st->part[0] = tot[0];
+                a.st->part[1] = 0.0;
+            } else {
+                // the Jacobian action was checked by its own operator
+                leja_decide(a.st, a.coef, a.mi, a.m, a.nk, tot[0], 0.0, false);
             }
         }
     }
@@ -356,8 +358,14 @@ __global__ void __launch_bounds__(TPB) k_power_norm(int64_t len, const double* _
         double tot[1];
         gather_partials<1>(work, gridDim.x, tot);
         if (threadIdx.x == 0) {
-            if (scaled) st->nv = sqrt(tot[0]);
-            else st->nw = sqrt(tot[0]);
+            if (st->defer) {
+                st->part[0] = tot[0];
+                st->part[1] = 0.0;
+            } else if (scaled) {
+                st->nv = sqrt(tot[0]);
+            } else {
+                st->nw = sqrt(tot[0]);
+            }
         }
     }
 }

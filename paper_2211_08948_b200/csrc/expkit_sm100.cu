@@ -504,7 +504,8 @@ int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu, const do
 }
 
 int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu, const double* k,
-                 double eps, double* out, ek_scalar_state* st, double* work, void* stream) {
+                 double eps, double* out, ek_scalar_state* st, double* work,
+                 const double* const* halo, void* stream) {
     if (!grid_ok(g)) return EK_ERR_INVALID;
     if (g->problem == EK_P_SEMILINEAR) {
         set_error("semilinear remainder runs through the generic path");
@@ -519,7 +520,7 @@ int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu, c
         return EK_ERR_UNSUPPORTED;
     }
     KArgs a;
-    base_args(a, g, nullptr);
+    base_args(a, g, halo);
     a.u = u; a.fu = fu; a.k = k; a.eps = eps; a.out = out; a.st = st; a.work = work;
     return launch_stencil<EP_REM>(ev, a, (cudaStream_t)stream);
 }
@@ -544,7 +545,7 @@ int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
 int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu, const double* b,
                 double* const* ybuf, double* const* p, int k, const double* coef_dev,
                 int chunk_base, int m_begin, int m_end, double gamma, ek_leja_state* st,
-                double* work, void* stream) {
+                double* work, const double* const* halo, void* stream) {
     if (!grid_ok(g)) return EK_ERR_INVALID;
     if (k < 1 || k > 8) {
         set_error("ek_leja_run: k=%d out of range", k);
@@ -554,7 +555,7 @@ int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu, co
     if (ev < 0) return EK_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     KArgs a;
-    base_args(a, g, nullptr);
+    base_args(a, g, halo);
     a.u = u; a.fu = fu; a.nk = k; a.coef = coef_dev; a.gamma = mkdv(gamma); a.st = st; a.work = work;
     for (int q = 0; q < k; ++q) a.p[q] = p[q];
     for (int m = m_begin; m < m_end; ++m) {
@@ -588,13 +589,16 @@ int ek_leja_update(int64_t len, const double* jv, const double* y, double* ynext
 // ------------------------------------------------------------------ power
 int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, const double* v0,
                  double* const* wbuf, int it_begin, int it_end, ek_power_state* st,
-                 double* work, void* stream) {
+                 double* work, const double* const* halo, void* stream) {
     if (!grid_ok(g)) return EK_ERR_INVALID;
     const int ev = jv_ev(g, jac);
     if (ev < 0) return EK_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t len = ek_grid_len(g);
-    if (it_begin == 0) {
+    // slab mode (halo given): only the stencil passes; the caller runs the
+    // norms (ek_power_norm) and the decisions (ek_power_decide) between them
+    const bool slab = halo != nullptr;
+    if (it_begin == 0 && !slab) {
         // v = v0 / ||v0||   (spectrum.py:49-51): divisor and, for FD, ||v||
         k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, v0, 0, st, work);
         EK_LAUNCH_CHECK("k_power_norm");
@@ -604,18 +608,41 @@ int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, c
         }
     }
     KArgs a;
-    base_args(a, g, nullptr);
+    base_args(a, g, halo);
     a.u = u; a.fu = fu; a.st = st; a.work = work;
     for (int it = it_begin; it < it_end; ++it) {
         a.y = it == 0 ? v0 : wbuf[(it - 1) & 1];
         a.out = wbuf[it & 1];
         const int rc = launch_stencil<EP_POWER>(ev, a, s);
         if (rc != EK_OK) return rc;
-        if (jac == EK_JAC_FD) {
+        if (jac == EK_JAC_FD && !slab) {
             k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, a.out, 1, st, work);
             EK_LAUNCH_CHECK("k_power_norm");
         }
     }
+    return EK_OK;
+}
+
+int ek_power_norm(int64_t len, const double* x, int scaled, ek_power_state* st, double* work,
+                  void* stream) {
+    k_power_norm<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(len, x, scaled, st, work);
+    EK_LAUNCH_CHECK("k_power_norm");
+    return EK_OK;
+}
+
+// ------------------------------------------------------- slab decisions
+int ek_leja_decide(ek_leja_state* st, const double* gathered, int nranks, const double* coef_dev,
+                   int chunk_base, int m, int k, int fd, int begin, void* stream) {
+    k_leja_decide<<<1, 32, 0, (cudaStream_t)stream>>>(st, gathered, nranks, coef_dev,
+                                                       m - chunk_base, m, k, fd, begin);
+    EK_LAUNCH_CHECK("k_leja_decide");
+    return EK_OK;
+}
+
+int ek_power_decide(ek_power_state* st, const double* gathered, int nranks, int fd, int which,
+                    void* stream) {
+    k_power_decide<<<1, 32, 0, (cudaStream_t)stream>>>(st, gathered, nranks, fd, which);
+    EK_LAUNCH_CHECK("k_power_decide");
     return EK_OK;
 }
 

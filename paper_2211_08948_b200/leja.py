@@ -173,6 +173,22 @@ class _CoefTable:
                 "coef upload")
 
 
+def _part_view(st):
+    """The 2-double `part` field of a device state block, as a tensor."""
+    off = type(st.host).part.offset
+    return st.buf[off:off + 16].view(D.F64)
+
+
+def _slab_decide(st, Jn, table, base, m, k, begin):
+    comm = Jn.comm
+    gathered = comm.allgather_pairs(_part_view(st))
+    N.check(N.lib().ek_leja_decide(st.ptr, C.c_void_p(gathered.data_ptr()), comm.world,
+                                   C.c_void_p(table.dev.data_ptr()), base, m, k,
+                                   1 if Jn.jac == N.JAC_FD else 0, 1 if begin else 0,
+                                   D.stream()), "ek_leja_decide")
+    return gathered
+
+
 def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                               xi=None, max_points=DEFAULT_NUM_POINTS):
     """phi_l(c_i h J) b for several scale factors c_i sharing one Newton
@@ -210,13 +226,16 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     Jn = fused[0] if fused else None
     nu = Jn.nu if Jn is not None and Jn.jac == N.JAC_FD else 0.0
 
+    slab = Jn is not None and Jn.comm is not None
     ps = [D.empty(n) for _ in range(k)]
-    st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k)
+    st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k, defer=1 if slab else 0)
     ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(Jn.grid)) if Jn else None)
     pp = N.ptrs(ps)
     N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()), pp, k,
                                       C.c_void_p(table.dev.data_ptr()), st.ptr, ws,
                                       D.stream()), "ek_leja_begin_len")
+    if slab:
+        _slab_decide(st, Jn, table, 0, 0, k, begin=True)
     if Jn is None or max_points <= 1:
         # a generic action must not run (and charge) after termination
         hst = st.read()
@@ -249,11 +268,24 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                 import torch
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
-            N.check(N.lib().ek_leja_run(
-                C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
-                C.c_void_p(Jn.fu.data_ptr()), C.c_void_p(bd.data_ptr()), yp, pp, k,
-                C.c_void_p(table.dev.data_ptr()), base, m, hi, float(gamma), st.ptr,
-                ws, D.stream()), "ek_leja_run")
+            if slab:
+                # per iteration: ghost rows of y_{m-1}, local fused pass,
+                # all-gather of the local sums, device decision (all ranks
+                # reach the same one, so they stay in lockstep)
+                for mm in range(m, hi):
+                    yprev = bd if mm == 1 else ybuf[(mm - 1) & 1]
+                    N.check(N.lib().ek_leja_run(
+                        C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
+                        C.c_void_p(Jn.fu.data_ptr()), C.c_void_p(bd.data_ptr()), yp, pp, k,
+                        C.c_void_p(table.dev.data_ptr()), base, mm, mm + 1, float(gamma),
+                        st.ptr, ws, Jn.halos(v=yprev), D.stream()), "ek_leja_run")
+                    _slab_decide(st, Jn, table, base, mm, k, begin=False)
+            else:
+                N.check(N.lib().ek_leja_run(
+                    C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
+                    C.c_void_p(Jn.fu.data_ptr()), C.c_void_p(bd.data_ptr()), yp, pp, k,
+                    C.c_void_p(table.dev.data_ptr()), base, m, hi, float(gamma), st.ptr,
+                    ws, None, D.stream()), "ek_leja_run")
             if prof is not None:
                 ev[1].record()
                 prof["events"].append(ev)

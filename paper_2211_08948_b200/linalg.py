@@ -200,6 +200,26 @@ class NativeJacobian(MatrixFreeOperator):
             self._nu = D.norm2(self.u)[0] if self.jac == N.JAC_FD else 0.0
         return self._nu
 
+    @property
+    def comm(self):
+        return self.stencil.comm
+
+    @property
+    def u_halo(self):
+        """Ghost rows of u (slab mode), exchanged once per linearisation."""
+        if getattr(self, "_uh", None) is None:
+            self._uh = self.stencil.halo(self.u)
+        return self._uh
+
+    def halos(self, v=None, k=None):
+        """C array {u, y, k} of halo buffers, or None off slab mode; the
+        buffers are kept on the object until the next call."""
+        if self.comm is None:
+            return None
+        self._hv = self.stencil.halo(v) if v is not None else None
+        self._hk = self.stencil.halo(k) if k is not None else None
+        return N.ptrs([self.u_halo, self._hv, self._hk])
+
     def apply(self, v):
         self._check(v)
         out = self.apply_dev(D.to_dev(v))
@@ -208,6 +228,7 @@ class NativeJacobian(MatrixFreeOperator):
     def apply_dev(self, v):
         self._check(v)
         out = D.empty(self.dim)
+        halo = self.halos(v=v)
         if self.jac == N.JAC_FD:
             nv, flag = D.norm2(v)
             if not flag & 1:  # `if not np.any(v)` (integrators.py:89)
@@ -221,15 +242,15 @@ class NativeJacobian(MatrixFreeOperator):
                                   C.c_void_p(self.fu.data_ptr()),
                                   C.c_void_p(v.data_ptr()), eps,
                                   C.c_void_p(out.data_ptr()), st.ptr, D.work_ptr(),
-                                  None, D.stream()), "ek_jv")
-            if st.read().flag & 2:
+                                  halo, D.stream()), "ek_jv")
+            if D.global_norm(st.read())[1] & 2:
                 raise FloatingPointError("non-finite Jacobian action")
             return out
         N.check(N.lib().ek_jv(C.byref(self.grid), N.JAC_ANALYTIC,
                               C.c_void_p(self.u.data_ptr()),
                               C.c_void_p(self.fu.data_ptr()),
                               C.c_void_p(v.data_ptr()), 0.0,
-                              C.c_void_p(out.data_ptr()), None, None, None,
+                              C.c_void_p(out.data_ptr()), None, None, halo,
                               D.stream()), "ek_jv")
         return out
 
@@ -263,7 +284,7 @@ def dot(x, y):
     N.check(N.lib().ek_vexpr(xd.numel(), code, len(pr.code), (C.c_double * 1)(), 0,
                              N.ptrs(pr.ins), len(pr.ins), N.ptrs([]), 0, st.ptr,
                              D.work_ptr(), D.stream()), "ek_vexpr")
-    return float(st.read().val[0])
+    return D.global_sum(float(st.read().val[0]))
 
 
 def axpy(alpha, x, y):

@@ -43,8 +43,15 @@ class StencilRhs:
         self.name = name
         self.grid = grid
         self.analytic = analytic
+        self.comm = None          # slab.SlabComm when this is a rank's slab
+        self.global_grid = None
         self.length = int(N.lib().ek_grid_len(C.byref(grid))) if N.lib_path().exists() \
             else None
+
+    def halo(self, x):
+        """Ghost rows of the local field x (slab mode): flat device buffer."""
+        from .slab import halo_buffer
+        return self.comm.exchange(x, self.grid, halo_buffer(self.grid))
 
     def __call__(self, u):
         ud = D.to_dev(u)
@@ -53,8 +60,12 @@ class StencilRhs:
         if ud.numel() != self.length:
             raise ValueError(f"{self.name}: state length {ud.numel()} != {self.length}")
         out = D.empty(self.length)
+        halo = None
+        if self.comm is not None:
+            hb = self.halo(ud)
+            halo = N.ptrs([hb, None, None])
         N.check(N.lib().ek_rhs(C.byref(self.grid), C.c_void_p(ud.data_ptr()),
-                               C.c_void_p(out.data_ptr()), None, D.stream()), "ek_rhs")
+                               C.c_void_p(out.data_ptr()), halo, D.stream()), "ek_rhs")
         return D.like_input(out, u)
 
 

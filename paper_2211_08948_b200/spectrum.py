@@ -69,8 +69,19 @@ _POWER_BATCH = 8
 def power_iterate(J: MatrixFreeOperator, tol_pi=1e-2, max_it=1000, seed=0):
     """Dominant |lambda| of J by power iteration (spectrum.py:43-63).
     Returns (estimate, converged)."""
-    v0 = _start_vector(seed, J.dim)
     fused = fused_target(J)
+    if fused is not None and fused[0].comm is not None:
+        # slab mode: this rank's rows of the global seeded start vector
+        sten = fused[0].stencil
+        key = (seed, "slab", sten.comm.rank, int(sten.grid.row0), J.dim)
+        v0 = _START.get(key)
+        if v0 is None:
+            glen = int(N.lib().ek_grid_len(C.byref(sten.global_grid)))
+            host = np.random.default_rng(seed).standard_normal(glen)
+            v0 = D.to_dev(sten.comm.scatter(host, sten.global_grid))
+            _START[key] = v0
+    else:
+        v0 = _start_vector(seed, J.dim)
     if fused is not None and fused[1] == 1.0 and fused[0].grid.problem != N.P_SEMILINEAR:
         return _power_fused(fused[0], v0, tol_pi, max_it)
     # generic operator: the action runs per iteration on the host's request
@@ -89,20 +100,57 @@ def power_iterate(J: MatrixFreeOperator, tol_pi=1e-2, max_it=1000, seed=0):
     return float(lam), False
 
 
+def _part(st):
+    off = type(st.host).part.offset
+    return st.buf[off:off + 16].view(D.F64)
+
+
+def _slab_decide(st, J, which):
+    g = J.comm.allgather_pairs(_part(st))
+    N.check(N.lib().ek_power_decide(st.ptr, C.c_void_p(g.data_ptr()), J.comm.world,
+                                    1 if J.jac == N.JAC_FD else 0, which, D.stream()),
+            "ek_power_decide")
+
+
+def _slab_norm(st, J, x, scaled, ws):
+    N.check(N.lib().ek_power_norm(x.numel(), C.c_void_p(x.data_ptr()), scaled, st.ptr, ws,
+                                  D.stream()), "ek_power_norm")
+    _slab_decide(st, J, 2 if scaled else 1)
+
+
 def _power_fused(J, v0, tol_pi, max_it):
-    st = D.DevState(N.PowerState, lam=0.0, nu=J.nu, tol_pi=tol_pi, max_it=max_it)
+    slab = J.comm is not None
+    st = D.DevState(N.PowerState, lam=0.0, nu=J.nu, tol_pi=tol_pi, max_it=max_it,
+                    defer=1 if slab else 0)
     wbuf = [D.empty(J.dim), D.empty(J.dim)]
     wp = N.ptrs(wbuf)
+    ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(J.grid)))
     it = 0
     h = None
     fd_seen = 0
+    fd = J.jac == N.JAC_FD
+    if slab:
+        # v = v0 / ||v0|| with the global norm (and ||v|| for the FD increment)
+        _slab_norm(st, J, v0, 0, ws)
+        if fd:
+            _slab_norm(st, J, v0, 1, ws)
     while it < max_it:
         hi = min(max_it, it + (_POWER_BATCH if it else 4))
-        N.check(N.lib().ek_power_run(
-            C.byref(J.grid), J.jac, C.c_void_p(J.u.data_ptr()),
-            C.c_void_p(J.fu.data_ptr()), C.c_void_p(v0.data_ptr()), wp, it, hi,
-            st.ptr, D.work_ptr(N.lib().ek_workspace_bytes(C.byref(J.grid))),
-            D.stream()), "ek_power_run")
+        if slab:
+            for i in range(it, hi):
+                vin = v0 if i == 0 else wbuf[(i - 1) & 1]
+                N.check(N.lib().ek_power_run(
+                    C.byref(J.grid), J.jac, C.c_void_p(J.u.data_ptr()),
+                    C.c_void_p(J.fu.data_ptr()), C.c_void_p(v0.data_ptr()), wp, i, i + 1,
+                    st.ptr, ws, J.halos(v=vin), D.stream()), "ek_power_run")
+                _slab_decide(st, J, 0)
+                if fd:
+                    _slab_norm(st, J, wbuf[i & 1], 1, ws)
+        else:
+            N.check(N.lib().ek_power_run(
+                C.byref(J.grid), J.jac, C.c_void_p(J.u.data_ptr()),
+                C.c_void_p(J.fu.data_ptr()), C.c_void_p(v0.data_ptr()), wp, it, hi,
+                st.ptr, ws, None, D.stream()), "ek_power_run")
         h = st.read()
         if J.jac == N.JAC_FD:
             J.rhs.counter.charge(h.fd_evals - fd_seen)

@@ -1,0 +1,172 @@
+"""Slab decomposition (multi-GPU path).
+
+CPU (gloo, world size 2): halo exchange for periodic and Neumann grids,
+rank-ordered sums, scatter / gather — the host logic of the N > 1 path.
+GPU: the slab code path at P = 1 reproduces the single-GPU path bit for bit,
+and two ranks sharing one GPU through host-staged gloo exchanges (no kernel
+waits on another rank's kernel) reproduce the single-GPU Leja / power
+iteration / EPIRK5P1 results with identical decisions.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2211_08948_b200 import _native as N
+from paper_2211_08948_b200 import slab as S
+from paper_2211_08948_b200.problems import make_grid
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _cpu_worker(rank, world, port, q):
+    _init(rank, world, port)
+    try:
+        comm = S.SlabComm()
+        out = {}
+        for bc in (N.BC_PERIODIC, N.BC_NEUMANN):
+            for ncomp in (1, 2):
+                n = 8
+                g = make_grid(N.P_BRUSS_STANDARD if ncomp == 2 else N.P_ALLEN_CAHN, bc, 2,
+                              ncomp, n, 1.0 / n)
+                glob = np.arange(ncomp * n * n, dtype=np.float64) * 1.5 + 7.0
+                loc = torch.from_numpy(comm.scatter(glob, g))
+                gl = S.slab_grid(g, comm)
+                halo = torch.zeros(2 * ncomp * n, dtype=torch.float64)
+                comm.exchange(loc, gl, halo)
+                out[(bc, ncomp)] = (int(gl.row0), int(gl.rows), halo.numpy().copy(),
+                                    comm.gather(loc.numpy(), g))
+        out["sum"] = comm.allsum([0.1 * (rank + 1), 1e-17 * rank])
+        part = torch.tensor([1.0 + rank, 2.0 * rank], dtype=torch.float64)
+        out["pairs"] = comm.allgather_pairs(part).numpy().copy()
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_halo_exchange_and_sums():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 8
+    for bc in (N.BC_PERIODIC, N.BC_NEUMANN):
+        for ncomp in (1, 2):
+            glob = (np.arange(ncomp * n * n, dtype=np.float64) * 1.5 + 7.0).reshape(ncomp, n, n)
+            for r in range(world):
+                row0, rows, halo, gathered = res[r][(bc, ncomp)]
+                assert rows == n // world and row0 == r * rows
+                assert np.array_equal(gathered, glob.reshape(-1))
+                lo = halo[:ncomp * n].reshape(ncomp, n)
+                hi = halo[ncomp * n:].reshape(ncomp, n)
+                up, down = row0 - 1, row0 + rows
+                if bc == N.BC_PERIODIC:
+                    up, down = up % n, down % n
+                else:  # np.pad 'reflect'
+                    up = 1 if up < 0 else up
+                    down = n - 2 if down >= n else down
+                assert np.array_equal(lo, glob[:, up, :])
+                assert np.array_equal(hi, glob[:, down, :])
+    for r in range(world):
+        assert res[r]["sum"] == [0.1 + 0.2, 0.0 + 1e-17]
+        assert np.array_equal(res[r]["pairs"], np.array([[1.0, 0.0], [2.0, 2.0]]))
+
+
+# ----------------------------------------------------------------- GPU
+
+def _gpu_run(local, n, comm=None):
+    """Power iteration + vertical Leja + one EPIRK5P1 step on the periodic
+    Brusselator, on the full grid (comm None) or this rank's slab."""
+    import paper_2211_08948_b200 as ek
+    from paper_2211_08948_b200 import ext
+    prob = ext.brusselator_periodic_problem(n=n)
+    if comm is not None:
+        prob = S.distribute(prob, comm)
+    xi = ek.get_leja_points(400)
+    rhs = ek.CountingRhs(prob.rhs)
+    sys_ = ek.make_linearized(rhs, prob.u0)
+    lam, conv = ek.power_iterate(sys_.J)
+    est = ek.make_estimate(lam)
+    dt = 40.0 / abs(est.alpha)
+    r = ek.leja_interpolate_vertical(sys_.J, sys_.f_n * dt, 1, [0.4, 1.0], dt, est, 1e-10, xi=xi)
+    st = ek.take_step("epirk5p1", sys_, dt, "leja", 1e-8, ek.EngineContext(est=est, xi=xi))
+    vecs = [sys_.f_n, *r.vectors, st.u_high]
+    if comm is not None:
+        g = prob.rhs.global_grid
+        vecs = [comm.gather(v, g) for v in vecs]
+    return {"lam": lam, "conv": conv, "iters": r.iters, "freeze": r.freeze_iters,
+            "step_iters": st.stats.leja_iters, "err": st.err_est,
+            "charges": rhs.counter.count, "vecs": vecs}
+
+
+@pytest.mark.gpu
+def test_slab_path_p1_bit_identical():
+    from paper_2211_08948_b200 import _device as D
+    a = _gpu_run(0, 96)
+    b = _gpu_run(0, 96, comm=S.SlabComm())
+    D.COMM = None
+    assert (a["iters"], a["freeze"], a["step_iters"], a["charges"]) == \
+        (b["iters"], b["freeze"], b["step_iters"], b["charges"])
+    assert a["lam"] == b["lam"] and a["err"] == b["err"]
+    for x, y in zip(a["vecs"], b["vecs"]):
+        assert np.array_equal(x, y)
+
+
+def _gpu_worker(rank, world, port, n, q):
+    _init(rank, world, port)
+    try:
+        torch.cuda.set_device(0)
+        out = _gpu_run(0, n, comm=S.SlabComm())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_ranks_match_single_gpu():
+    n = 128
+    ref = _gpu_run(0, n)
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        got = res[r]
+        assert (got["iters"], got["freeze"], got["step_iters"], got["charges"]) == \
+            (ref["iters"], ref["freeze"], ref["step_iters"], ref["charges"])
+        assert got["lam"] == pytest.approx(ref["lam"], rel=1e-13)
+        assert np.array_equal(got["vecs"][0], ref["vecs"][0])   # RHS: bit-exact
+        for x, y in zip(got["vecs"][1:], ref["vecs"][1:]):
+            assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y)
+    # both ranks hold the same gathered results
+    for x, y in zip(res[0]["vecs"], res[1]["vecs"]):
+        assert np.array_equal(x, y)
