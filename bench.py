@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_GRID)
+    ap.add_argument("--grid", type=int, default=N_GRID)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -169,15 +169,21 @@ def run_ours(args, rank, world, local):
     from paper_2211_08948_b200 import ext, _native as N, _device as D
     from paper_2211_08948_b200 import leja as L
 
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    n = args.n
+    n = args.grid
     prob = ext.brusselator_periodic_problem(n=n)
     if world > 1:
         # strong scaling: the global 4096^2 x 2 grid in row slabs, NCCL halos
-        # and rank-ordered reductions (paper_2211_08948_b200/slab.py)
+        # and rank-ordered reductions (paper_2211_08948_b200/slab.py).
+        # EK_BENCH_BACKEND=gloo exercises the same path host-staged (tests).
         import torch.distributed as dist
         from paper_2211_08948_b200 import slab as SL
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("EK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         prob = SL.distribute(prob, SL.SlabComm())
     xi = ek.get_leja_points(400)
     rhs = ek.CountingRhs(prob.rhs)
@@ -382,7 +388,7 @@ def run_reference(args, rank, world):
     restatement), one FD Leja iteration per step, same config / metric."""
     if rank != 0:
         return None
-    n = args.n
+    n = args.grid
     OP, sys_, rhs = _oracle_setup(n)
     xi = OP.leja_points(400)
     # the same stiffness window as our arm: dt |alpha| = 50 with alpha from a
