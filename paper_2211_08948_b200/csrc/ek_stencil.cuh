@@ -371,9 +371,23 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
 #pragma unroll
         for (int t = 0; t < 5; ++t)
             ctl.augc[t] = t < a.naug ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
+        // centre slots: window rows, then augmentation vectors; d[q] holds
+        // the tail coefficient of augmentation slot q
+        ctl.active = (1u << (a.nwin + a.naug)) - 1u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int t = q - a.nwin;
+            ctl.d[q] = (t >= 0 && t < a.naug)
+                           ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
+        }
     }
     ctl.eps_d = mkdv(ctl.eps);
     return true;
+}
+
+// EP_ARN centre slot q: window row q (q < nwin), else augmentation q - nwin
+__host__ __device__ __forceinline__ const double* arn_slot(const KArgs& a, int q) {
+    return q < a.nwin ? a.win[q] : a.aug[q - a.nwin];
 }
 
 // Centre values loaded with the neighbourhood, before any store.
@@ -397,6 +411,10 @@ __device__ __forceinline__ void load_centre(const KArgs& a, const Ctl& ctl, long
 #pragma unroll
             for (int q = 0; q < K; ++q)
                 z.p[q][c] = ((ctl.active >> q) & 1u) ? a.p[q][e] : 0.0;
+        } else if constexpr (EP == EP_ARN) {
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                z.p[q][c] = ((ctl.active >> q) & 1u) ? __ldg(arn_slot(a, q) + e) : 0.0;
         }
     }
 }
@@ -429,15 +447,16 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
         } else if constexpr (EP == EP_ARN) {
             // V[j,:n] = op.apply(V[j-1,:n]) + V[j-1,n:] @ u_flip    kiops.py:182
+            // centre slots (z.p): window rows [0, nwin), augmentation [nwin, nwin+naug)
             double augv = 0.0;
 #pragma unroll
-            for (int t = 0; t < 5; ++t)
-                if (t < a.naug) augv = augv + (ctl.augc[t] * __ldg(a.aug[t] + e));
+            for (int q = 0; q < K; ++q)
+                if (q >= a.nwin && q < a.nwin + a.naug) augv = augv + (ctl.d[q] * z.p[q][c]);
             const double w = (a.dt * v) + augv;
             a.out[e] = w;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (q < a.nwin) acc[q] += __ldg(a.win[q] + e) * w;
+            for (int q = 0; q < (K < 4 ? K : 4); ++q)
+                if (q < a.nwin) acc[q] += z.p[q][c] * w;
             if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
         } else {  // EP_REM
             a.out[e] = v;

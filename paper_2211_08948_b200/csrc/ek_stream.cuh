@@ -101,10 +101,11 @@ __device__ __forceinline__ void make_ch(const Ctl& ctl, const double (&r)[NR], d
     }
 }
 
-// centre maps: f(u_n) (if used) then the K accumulators
+// centre maps: f(u_n) (if used) then K more: the Leja accumulators, or the
+// Arnoldi window rows followed by the augmentation vectors
 template <int EV, int EP, int K>
 __host__ __device__ constexpr int nctr_maps() {
-    return (needs_fu<EV>() ? 1 : 0) + (EP == EP_LEJA ? K : 0);
+    return (needs_fu<EV>() ? 1 : 0) + ((EP == EP_LEJA || EP == EP_ARN) ? K : 0);
 }
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage_doubles() {
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 z.fu[c] = FU ? ctr[c * CTR_SLOT + co] : 0.0;
-                if constexpr (EP == EP_LEJA) {
+                if constexpr (EP == EP_LEJA || EP == EP_ARN) {
                     z.y[c] = yc[c];
 #pragma unroll
                     for (int q = 0; q < K; ++q)

@@ -278,6 +278,11 @@ static bool build_maps(const KArgs& a, TmaMaps& m) {
     if constexpr (EP == EP_LEJA)
         for (int q = 0; q < K && q < a.nk; ++q)
             if (!tensor_map(&m.m[t++], a.p[q], cols, rt, 32, 8)) return false;
+    if constexpr (EP == EP_ARN)
+        for (int q = 0; q < K && q < a.nwin + a.naug; ++q) {
+            const double* f = arn_slot(a, q);
+            if (!al16(f) || !tensor_map(&m.m[t++], f, cols, rt, 32, 8)) return false;
+        }
     return true;
 }
 
@@ -322,6 +327,14 @@ template <class P, int EV, int EP>
 static int launch_p(const KArgs& a, cudaStream_t s) {
     if constexpr (EP == EP_LEJA) {
         switch (a.nk) {
+            case 1: return launch_k<P, EV, EP, 1>(a, s);
+            case 2: return launch_k<P, EV, EP, 2>(a, s);
+            case 3: return launch_k<P, EV, EP, 3>(a, s);
+            default: return launch_k<P, EV, EP, 8>(a, s);
+        }
+    } else if constexpr (EP == EP_ARN) {
+        // centre slots = window rows + nonzero augmentation vectors
+        switch (a.nwin + a.naug) {
             case 1: return launch_k<P, EV, EP, 1>(a, s);
             case 2: return launch_k<P, EV, EP, 2>(a, s);
             case 3: return launch_k<P, EV, EP, 3>(a, s);
@@ -676,7 +689,7 @@ int ek_arnoldi_run(const ek_grid* g, int jac, const double* u, const double* fu,
                    double aug_scale, int j_begin, int j_end, double* H, ek_arnoldi_state* st, int p, int iop,
                    int ldh, double dt, double* work, void* stream) {
     if (!grid_ok(g)) return EK_ERR_INVALID;
-    if (iop < 1 || iop > 4 || p < 1 || p > 5 || naug > 5) {
+    if (iop < 1 || iop > 4 || p < 1 || p > 5 || naug > 5 || iop + naug > 8) {
         set_error("ek_arnoldi_run: iop=%d p=%d naug=%d out of range", iop, p, naug);
         return EK_ERR_INVALID;
     }

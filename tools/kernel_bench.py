@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--problem", default="brusselator_periodic")
     ap.add_argument("--no-tma", action="store_true")
+    ap.add_argument("--kiops", action="store_true")
     args = ap.parse_args()
 
     import torch
@@ -58,11 +59,39 @@ def main():
     t = sum(s.elapsed_time(e) for s, e in prof[0]["events"]) / 1e3
     n = sys_._u.numel()
     fd = prof[0]["fd"]
-    per = 8 * n * ((4 if fd else 2) + 2 * args.k)
+    lin = args.problem in ("advdiff2d", "advdiff3d")
+    base = 4 if fd else (2 if lin else 3)
+    per = 8 * n * (base + 2 * args.k)
     out = {"problem": args.problem, "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
            "ms_per_launch": t / args.iters * 1e3, "bytes_per_launch": per,
            "GBps": per * args.iters / t / 1e9}
     print(json.dumps(out))
+    if args.kiops:
+        # KIOPS Arnoldi steps on the same operator: one substep of m steps
+        K = ek
+        vecs = [None, b]
+        try:
+            K.kiops(sys_.J.scaled(dt), vecs, tol=1e-300, m_init=4, m_min=4, m_max=4,
+                    tau_min_frac=0.5)
+        except ek.NonConvergence:
+            pass
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        try:
+            _, st = K.kiops(sys_.J.scaled(dt), vecs, tol=1e-300, m_init=args.iters,
+                            m_min=args.iters, m_max=args.iters, tau_min_frac=0.5)
+        except ek.NonConvergence as exc:
+            st = None
+            del exc
+        e1.record()
+        torch.cuda.synchronize()
+        tk = e0.elapsed_time(e1) / 1e3
+        # per Arnoldi step (FD, p_nz = 1): pass A 8N(5+1), B 8N*4, C 8N*2 (n+p ~ n)
+        perk = 8 * n * ((4 if fd else (2 if lin else 3)) + 1 + 1 + 1 + 4 + 2)
+        print(json.dumps({"kiops_steps": args.iters, "ms_per_arnoldi_step_incl_host":
+                          tk / args.iters * 1e3, "bytes_per_step": perk,
+                          "GBps_incl_host": perk * args.iters / tk / 1e9}))
 
 
 if __name__ == "__main__":
