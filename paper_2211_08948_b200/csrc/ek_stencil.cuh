@@ -373,7 +373,9 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
             ctl.augc[t] = t < a.naug ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
         // centre slots: window rows, then augmentation vectors; d[q] holds
         // the tail coefficient of augmentation slot q
-        ctl.active = (1u << (a.nwin + a.naug)) - 1u;
+        // (bits = slots fetched from memory; slot nwin-1 is V[j-1] = y itself,
+        // whose centre value the streaming kernel already holds)
+        ctl.active = ((1u << (a.nwin + a.naug)) - 1u) & ~(1u << (a.nwin - 1));
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int t = q - a.nwin;
@@ -414,7 +416,7 @@ __device__ __forceinline__ void load_centre(const KArgs& a, const Ctl& ctl, long
         } else if constexpr (EP == EP_ARN) {
 #pragma unroll
             for (int q = 0; q < K; ++q)
-                z.p[q][c] = ((ctl.active >> q) & 1u) ? __ldg(arn_slot(a, q) + e) : 0.0;
+                z.p[q][c] = q < a.nwin + a.naug ? __ldg(arn_slot(a, q) + e) : 0.0;
         }
     }
 }

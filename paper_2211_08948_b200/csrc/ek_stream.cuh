@@ -5,7 +5,9 @@
 // (`cp.async.bulk.tensor.2d`, completion counted in bytes on an mbarrier),
 // S stages deep. One thread issues a handful of box copies per chunk; the
 // data in flight lives in shared memory, not registers, so a block keeps
-// S-1 chunks (~60 KB) of HBM reads outstanding while it computes one.
+// up to S chunks (~80-110 KB) of HBM reads outstanding. Stages are released
+// per warp (mbarrier arrivals), so the warps of a block never wait for each
+// other, and interior chunks take a branch-free path with no ghost logic.
 //
 // Chunk = 32 columns x 8 rows (one row per warp). Per stage:
 //   raw[f][c]  box of 10 x 36 doubles: rows r0-1..r0+8, columns j0-2..j0+33
@@ -154,23 +156,106 @@ __device__ __forceinline__ void issue_chunk(const TmaMaps& maps, double* buf, ui
     }
 }
 
+// One grid point (i, j) of chunk stage `raw`/`ctr`. EDGE = the chunk touches
+// the domain boundary, so ghost rows/columns may come from global memory;
+// interior chunks (the vast majority) read everything from the stage.
+template <class P, int EV, int EP, int K, bool EDGE>
+__device__ __forceinline__ void tma_point(const KArgs& a, const Ctl& ctl, const double* raw,
+                                          const double* ctr, const double* const (&rb)[2],
+                                          const double* const (&rh)[2], int i, int j, int wid,
+                                          int lane, int rows, int cols, double* acc) {
+    constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
+    constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    const bool gx_m = EDGE && i == 0, gx_p = EDGE && i == rows - 1;  // ghost rows (warp-uniform)
+    const bool gy_m = EDGE && j == 0, gy_p = EDGE && j == cols - 1;  // ghost columns
+    Nb nb[NC][NCH];
+    double yc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        double rc[NR], rxm[NR], rxp[NR], rym[NR], ryp[NR];
+#pragma unroll
+        for (int f = 0; f < NR; ++f) {
+            const double* bx = raw + (f * NC + c) * RAW_SLOT + (1 + wid) * TBW + 2 + lane;
+            rc[f] = bx[0];
+            if constexpr (EDGE) {
+                rxm[f] = gx_m ? __ldg(slab_row(a, rb[f], rh[f], c, -1, cols) + j) : bx[-TBW];
+                rxp[f] = gx_p ? __ldg(slab_row(a, rb[f], rh[f], c, rows, cols) + j) : bx[TBW];
+                const double* rowg = rb[f] + c * a.npts + (long)i * cols;
+                rym[f] = gy_m ? __ldg(rowg + wrap_idx(-1, cols, a.g.bc)) : bx[-1];
+                ryp[f] = gy_p ? __ldg(rowg + wrap_idx(cols, cols, a.g.bc)) : bx[1];
+            } else {
+                rxm[f] = bx[-TBW];
+                rxp[f] = bx[TBW];
+                rym[f] = bx[-1];
+                ryp[f] = bx[1];
+            }
+        }
+        yc[c] = rc[yraw<EV>() < NR ? yraw<EV>() : 0];
+        double hc[NCH], hxm[NCH], hxp[NCH], hym[NCH], hyp[NCH];
+        make_ch<EV, NCH, NR>(ctl, rc, hc);
+        make_ch<EV, NCH, NR>(ctl, rxm, hxm);
+        make_ch<EV, NCH, NR>(ctl, rxp, hxp);
+        make_ch<EV, NCH, NR>(ctl, rym, hym);
+        make_ch<EV, NCH, NR>(ctl, ryp, hyp);
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) nb[c][h] = Nb{hc[h], hxm[h], hxp[h], hym[h], hyp[h], 0.0, 0.0};
+    }
+    Centre<EV, EP, NC, K> z;
+    const int co = wid * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        z.fu[c] = FU ? ctr[c * CTR_SLOT + co] : 0.0;
+        if constexpr (EP == EP_LEJA || EP == EP_ARN) {
+            z.y[c] = yc[c];
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                z.p[q][c] = (EP == EP_ARN && q == a.nwin - 1)
+                                ? yc[c] : ctr[((FU + q) * NC + c) * CTR_SLOT + co];
+        }
+    }
+    double val[NC];
+    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
+    epilogue<EV, EP, NC, K>(a, ctl, (long)i * cols + j, val, z, acc);
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Pipeline: full[s] counts the bytes of the chunk in stage s; empty[s] the
+// 8 warps that released it. Thread 0 is the producer: before consuming
+// chunk k it makes sure chunk k has been issued (blocking on the release of
+// chunk k-S only if that is the oldest one still missing) and then issues as
+// many further chunks as have free stages, without waiting. Warps never
+// synchronise with each other, only with the copies they consume.
 template <class P, int EV, int EP, int K, int S>
 __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_constant__ TmaMaps maps) {
-    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
     constexpr int NR = nraw<EV>();
     constexpr int SD = stage_doubles<EV, EP, NC, K>();
-    constexpr int FU = needs_fu<EV>() ? 1 : 0;
     extern __shared__ __align__(1024) double smem[];
-    __shared__ __align__(8) uint64_t bars[S];
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ __align__(8) uint64_t empty[S];
 
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cols = (int)a.g.n, rows = (int)a.g.rows;
     const int tiles_c = (cols + 31) / 32;
-    const long nchunks = (long)tiles_c * ((rows + 7) / 8);
-    const long G = gridDim.x;
-    const long my = nchunks > (long)blockIdx.x ? (nchunks - 1 - blockIdx.x) / G + 1 : 0;
+    const int nchunks = tiles_c * ((rows + 7) / 8);
+    const int G = gridDim.x;
+    const int my = nchunks > (int)blockIdx.x ? (nchunks - 1 - (int)blockIdx.x) / G + 1 : 0;
     const double* rb[2];
     const double* rh[2];
     raw_fields<EV>(a, rb, rh);
@@ -179,14 +264,11 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
 #pragma unroll
         for (int t = 0; t < NR + nctr_maps<EV, EP, K>(); ++t)
             asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&maps.m[t]) : "memory");
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (long k = 0; k < S - 1 && k < my; ++k) {
-            const long t = blockIdx.x + k * G;
-            issue_chunk<EV, EP, NC, K>(maps, smem + (k % S) * SD, &bars[k % S],
-                                       (int)(t % tiles_c) * 32, (int)(t / tiles_c) * 8, rows,
-                                       ctl.active);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NWARP);
         }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
@@ -194,67 +276,35 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
-    for (long k = 0; k < my; ++k) {
-        if (threadIdx.x == 0 && k + S - 1 < my) {
-            // refill the stage freed at the end of iteration k-1
-            const long t = blockIdx.x + (k + S - 1) * G;
-            const int ns = (int)((k + S - 1) % S);
-            issue_chunk<EV, EP, NC, K>(maps, smem + ns * SD, &bars[ns], (int)(t % tiles_c) * 32,
-                                       (int)(t / tiles_c) * 8, rows, ctl.active);
+    int issued = 0;  // producer (thread 0) only
+    for (int k = 0; k < my; ++k) {
+        if (threadIdx.x == 0) {
+            while (issued < my && issued < k + S) {
+                const int s = issued % S;
+                if (issued >= S) {
+                    const uint32_t par = (uint32_t)((issued / S - 1) & 1);
+                    if (issued <= k) mbar_wait(&empty[s], par);
+                    else if (!mbar_test(&empty[s], par)) break;
+                }
+                const int t = (int)blockIdx.x + issued * G;
+                issue_chunk<EV, EP, NC, K>(maps, smem + s * SD, &full[s], (t % tiles_c) * 32,
+                                           (t / tiles_c) * 8, rows, ctl.active);
+                ++issued;
+            }
         }
-        const int s = (int)(k % S);
-        const long t = blockIdx.x + k * G;
-        const int j0 = (int)(t % tiles_c) * 32, r0 = (int)(t / tiles_c) * 8;
+        const int s = k % S;
+        const int t = (int)blockIdx.x + k * G;
+        const int j0 = (t % tiles_c) * 32, r0 = (t / tiles_c) * 8;
         const int i = r0 + wid, j = j0 + lane;
-        mbar_wait(&bars[s], (uint32_t)((k / S) & 1));
-        if (i < rows && j < cols) {
-            const double* raw = smem + s * SD;
-            const double* ctr = raw + NR * NC * RAW_SLOT;
-            const bool gx_m = i == 0, gx_p = i == rows - 1;   // ghost rows (warp-uniform)
-            const bool gy_m = j == 0, gy_p = j == cols - 1;   // ghost columns
-            Nb nb[NC][NCH];
-            double yc[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                double rc[NR], rxm[NR], rxp[NR], rym[NR], ryp[NR];
-#pragma unroll
-                for (int f = 0; f < NR; ++f) {
-                    const double* bx = raw + (f * NC + c) * RAW_SLOT + (1 + wid) * TBW + 2 + lane;
-                    rc[f] = bx[0];
-                    rxm[f] = gx_m ? __ldg(slab_row(a, rb[f], rh[f], c, -1, cols) + j) : bx[-TBW];
-                    rxp[f] = gx_p ? __ldg(slab_row(a, rb[f], rh[f], c, rows, cols) + j) : bx[TBW];
-                    const double* rowg = rb[f] + c * a.npts + (long)i * cols;
-                    rym[f] = gy_m ? __ldg(rowg + wrap_idx(-1, cols, a.g.bc)) : bx[-1];
-                    ryp[f] = gy_p ? __ldg(rowg + wrap_idx(cols, cols, a.g.bc)) : bx[1];
-                }
-                yc[c] = rc[yraw<EV>() < NR ? yraw<EV>() : 0];
-                double hc[NCH], hxm[NCH], hxp[NCH], hym[NCH], hyp[NCH];
-                make_ch<EV, NCH, NR>(ctl, rc, hc);
-                make_ch<EV, NCH, NR>(ctl, rxm, hxm);
-                make_ch<EV, NCH, NR>(ctl, rxp, hxp);
-                make_ch<EV, NCH, NR>(ctl, rym, hym);
-                make_ch<EV, NCH, NR>(ctl, ryp, hyp);
-#pragma unroll
-                for (int h = 0; h < NCH; ++h)
-                    nb[c][h] = Nb{hc[h], hxm[h], hxp[h], hym[h], hyp[h], 0.0, 0.0};
-            }
-            Centre<EV, EP, NC, K> z;
-            const int co = wid * 32 + lane;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                z.fu[c] = FU ? ctr[c * CTR_SLOT + co] : 0.0;
-                if constexpr (EP == EP_LEJA || EP == EP_ARN) {
-                    z.y[c] = yc[c];
-#pragma unroll
-                    for (int q = 0; q < K; ++q)
-                        z.p[q][c] = ctr[((FU + q) * NC + c) * CTR_SLOT + co];
-                }
-            }
-            double val[NC];
-            evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
-            epilogue<EV, EP, NC, K>(a, ctl, (long)i * cols + j, val, z, acc);
-        }
-        __syncthreads();  // every warp is done with stage s before it is refilled
+        const double* raw = smem + s * SD;
+        const double* ctr = raw + NR * NC * RAW_SLOT;
+        mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+        if (r0 >= 1 && r0 + 8 < rows && j0 >= 1 && j0 + 32 < cols)
+            tma_point<P, EV, EP, K, false>(a, ctl, raw, ctr, rb, rh, i, j, wid, lane, rows, cols, acc);
+        else if (i < rows && j < cols)
+            tma_point<P, EV, EP, K, true>(a, ctl, raw, ctr, rb, rh, i, j, wid, lane, rows, cols, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     }
     reduce_and_finalize<EV, EP, NQ>(a, acc);
 }
