@@ -57,6 +57,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+// Same with an L2 eviction-priority hint (createpolicy), for streams read once.
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y,
+                                                 uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
@@ -151,7 +165,8 @@ __device__ __forceinline__ void issue_chunk(const TmaMaps& maps, double* buf, ui
         if (g < FU || ((active >> (g - FU)) & 1u)) {
 #pragma unroll
             for (int c = 0; c < NC; ++c)
-                tma_load_2d(ctr + (g * NC + c) * CTR_SLOT, &maps.m[NR + g], j0, c * rows + r0, bar);
+                tma_load_2d_hint(ctr + (g * NC + c) * CTR_SLOT, &maps.m[NR + g], j0, c * rows + r0,
+                                 bar, policy_evict_first());
         }
     }
 }
