@@ -41,9 +41,9 @@ __device__ __forceinline__ long nblocks() {
 }
 
 // Sum NQ values over the block; the totals land in thread 0.
-template <int NQ>
+template <int NQ, int NW = NWARP>
 __device__ __forceinline__ void block_sum(double (&v)[NQ]) {
-    __shared__ double sh[NQ][NWARP];
+    __shared__ double sh[NQ][NW];
     const int t = flat_tid(), lane = t & 31, w = t >> 5;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -59,7 +59,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ]) {
     if (w == 0) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            double x = lane < NWARP ? sh[q][lane] : 0.0;
+            double x = lane < NW ? sh[q][lane] : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
             v[q] = x;
@@ -90,16 +90,16 @@ __device__ __forceinline__ bool publish_and_arrive(const double (&v)[NQ], double
 
 // In the last block: totals of the NQ partial channels, fixed order.
 // Result valid in thread 0.
-template <int NQ>
+template <int NQ, int NT = TPB>
 __device__ __forceinline__ void gather_partials(const double* work, long nb, double (&tot)[NQ]) {
     const int t = flat_tid();
 #pragma unroll
     for (int q = 0; q < NQ; ++q) tot[q] = 0.0;
-    for (long b = t; b < nb; b += TPB) {
+    for (long b = t; b < nb; b += NT) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) tot[q] += __ldcg(work + b * NQ + q);
     }
-    block_sum<NQ>(tot);
+    block_sum<NQ, NT / 32>(tot);
 }
 
 // Division by a launch-uniform divisor: reciprocal r = RN(1/d) plus one

@@ -479,13 +479,13 @@ __device__ __forceinline__ uint32_t* ticket_of(const KArgs& a) {
     else return &((ek_scalar_state*)a.st)->ticket;
 }
 
-template <int EV, int EP, int NQ>
+template <int EV, int EP, int NQ, int NT = TPB>
 __device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc)[NQ]) {
     if constexpr (ep_nq(EP) > 0) {
-        block_sum<NQ>(acc);
+        block_sum<NQ, NT / 32>(acc);
         if (publish_and_arrive<NQ>(acc, a.work, ticket_of<EP>(a))) {
             double tot[NQ];
-            gather_partials<NQ>(a.work, nblocks(), tot);
+            gather_partials<NQ, NT>(a.work, nblocks(), tot);
             if (flat_tid() == 0) finalize<EV, EP>(a, tot);
         }
     }

@@ -36,6 +36,7 @@ constexpr int MAX_MAPS = 11;     // 2 raw + f(u) + 8 accumulators
 
 struct TmaMaps {
     CUtensorMap m[MAX_MAPS];     // [0, nraw) raw fields, then f(u), then p_q
+    CUtensorMap h[2];            // 3-D slab: halo buffers of the raw fields
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

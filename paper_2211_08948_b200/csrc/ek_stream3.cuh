@@ -1,0 +1,296 @@
+// ek_stream3.cuh — TMA-pipelined 3-D stencil kernel (sm_100a).
+//
+// Same value / epilogue algebra as ek_stencil.cuh (k_stencil3d), staged by
+// 3-D tensor copies (`cp.async.bulk.tensor.3d`). Layout: flat index
+// i*n*n + jy*n + kx, axis 0 (i, the slab axis) outermost; a tensor map views
+// a field as (ncomp*rows) x n x n, so component c starts at plane c*rows.
+//
+// Work item = 64 (kx) x 16 (jy) columns x SEG3 consecutive planes of axis 0.
+// A block marches the planes of an item in order; one pipeline stage holds
+// one plane of the item: per raw field an 18 x 68 box (jy0-1..jy0+16,
+// kx0-2..kx0+65) and per centre field (f(u), accumulators, Arnoldi slots) a
+// 16 x 64 box; 16 warps, each thread computes 2 points of the plane. Plane i is computed from stages i-1, i, i+1, so every raw
+// plane is fetched once per item (plus the two ghost planes at its ends)
+// and the axis-0 neighbours cost no extra traffic. Ghost planes outside the
+// domain are fetched by the copy engine too: the wrapped / reflected plane
+// for a whole domain, the halo buffer (its own tensor map) for a slab.
+// Ghost rows / columns of axes 1 and 2 (x-y boundary of the item) are read
+// from global memory by the lanes that need them (EDGE items only).
+//
+// Pipeline: full[s] counts the bytes of the plane in stage s; a shared
+// counter the warps that released it. The last warp to release a stage
+// refills it with the plane S sequence numbers ahead, so copies are issued
+// the moment a stage frees up and no warp ever waits for another one.
+#pragma once
+
+#include "ek_stream.cuh"
+
+namespace ek {
+
+constexpr int SEG3 = 32;  // planes per work item
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int x, int y,
+                                                 int z, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+// Item geometry: I3X columns (kx) x I3Y rows (jy); raw boxes carry one
+// ghost row above/below and two columns left/right (16-byte multiples).
+constexpr int I3X = 64, I3Y = 16;
+constexpr int TBW3 = I3X + 4, TBR3 = I3Y + 2;
+constexpr int RAW3 = 1232;            // >= TBW3*TBR3 (1224), 128-B multiple
+constexpr int CTR3 = I3X * I3Y;       // 1024
+template <int EV, int EP, int NC, int K>
+__host__ __device__ constexpr int stage3_doubles() {
+    return nraw<EV>() * NC * RAW3 + nctr_maps<EV, EP, K>() * NC * CTR3;
+}
+
+struct Item3 {
+    int k0, j0, i0, L;
+};
+__device__ __forceinline__ Item3 item3(long t, int n, int rows) {
+    const int tk = (n + I3X - 1) / I3X, tj = (n + I3Y - 1) / I3Y;
+    Item3 it;
+    it.k0 = (int)(t % tk) * I3X;
+    it.j0 = (int)((t / tk) % tj) * I3Y;
+    it.i0 = (int)(t / ((long)tk * tj)) * SEG3;
+    it.L = rows - it.i0 < SEG3 ? rows - it.i0 : SEG3;
+    return it;
+}
+
+// Thread 0: issue position `pos` (plane i0 - 1 + pos) of item `it`.
+template <int EV, int EP, int NC, int K>
+__device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps, double* buf,
+                                            uint64_t* bar, const Item3& it, int pos, int rows,
+                                            uint32_t active) {
+    constexpr int NR = nraw<EV>(), NCM = nctr_maps<EV, EP, K>();
+    constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    const int i = it.i0 - 1 + pos;
+    const bool centre = pos >= 1 && pos <= it.L;
+    uint32_t bytes = NR * NC * (TBW3 * TBR3 * 8);
+    if (centre) {
+#pragma unroll
+        for (int g = 0; g < NCM; ++g)
+            if (g < FU || ((active >> (g - FU)) & 1u)) bytes += NC * (CTR3 * 8);
+    }
+    mbar_arrive_expect(bar, bytes);
+    const bool in = i >= 0 && i < rows;
+#pragma unroll
+    for (int f = 0; f < NR; ++f)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            double* dst = buf + (f * NC + c) * RAW3;
+            if (in) {
+                tma_load_3d(dst, &maps.m[f], it.k0 - 2, it.j0 - 1, c * rows + i, bar);
+            } else if (a.g.slab) {  // halo buffer [2][ncomp][plane]
+                tma_load_3d(dst, &maps.h[f], it.k0 - 2, it.j0 - 1, (i < 0 ? 0 : NC) + c, bar);
+            } else {
+                const int w = (int)wrap_idx(i, rows, a.g.bc);
+                tma_load_3d(dst, &maps.m[f], it.k0 - 2, it.j0 - 1, c * rows + w, bar);
+            }
+        }
+    if (centre) {
+        double* ctr = buf + NR * NC * RAW3;
+        const uint64_t pol = policy_evict_first();
+#pragma unroll
+        for (int g = 0; g < NCM; ++g)
+            if (g < FU || ((active >> (g - FU)) & 1u)) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    tma_load_3d_hint(ctr + (g * NC + c) * CTR3, &maps.m[NR + g], it.k0, it.j0,
+                                     c * rows + i, bar, pol);
+            }
+    }
+}
+
+// One point (i, jy, kx) from the stages of planes i-1 (pm), i (pc), i+1 (pp);
+// ro / co: its offset inside a raw / centre slot.
+template <class P, int EV, int EP, int K, bool EDGE>
+__device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const double* pm,
+                                           const double* pc, const double* pp,
+                                           const double* const (&rb)[2], long i, int jy, int kx,
+                                           int ro, int co, int n, double* acc) {
+    constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
+    constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    const long plane = (long)n * n;
+    const bool gy_m = EDGE && jy == 0, gy_p = EDGE && jy == n - 1;
+    const bool gz_m = EDGE && kx == 0, gz_p = EDGE && kx == n - 1;
+    Nb nb[NC][NCH];
+    double yc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        double rc[NR], rxm[NR], rxp[NR], rym[NR], ryp[NR], rzm[NR], rzp[NR];
+#pragma unroll
+        for (int f = 0; f < NR; ++f) {
+            const int o = (f * NC + c) * RAW3 + ro;
+            const double* bx = pc + o;
+            rc[f] = bx[0];
+            rxm[f] = pm[o];
+            rxp[f] = pp[o];
+            if constexpr (EDGE) {
+                const double* pl = rb[f] + c * a.npts + i * plane;
+                rym[f] = gy_m ? __ldg(pl + wrap_idx(-1, n, a.g.bc) * n + kx) : bx[-TBW3];
+                ryp[f] = gy_p ? __ldg(pl + wrap_idx(n, n, a.g.bc) * n + kx) : bx[TBW3];
+                rzm[f] = gz_m ? __ldg(pl + (long)jy * n + wrap_idx(-1, n, a.g.bc)) : bx[-1];
+                rzp[f] = gz_p ? __ldg(pl + (long)jy * n + wrap_idx(n, n, a.g.bc)) : bx[1];
+            } else {
+                rym[f] = bx[-TBW3];
+                ryp[f] = bx[TBW3];
+                rzm[f] = bx[-1];
+                rzp[f] = bx[1];
+            }
+        }
+        yc[c] = rc[yraw<EV>() < NR ? yraw<EV>() : 0];
+        double hc[NCH], hxm[NCH], hxp[NCH], hym[NCH], hyp[NCH], hzm[NCH], hzp[NCH];
+        make_ch<EV, NCH, NR>(ctl, rc, hc);
+        make_ch<EV, NCH, NR>(ctl, rxm, hxm);
+        make_ch<EV, NCH, NR>(ctl, rxp, hxp);
+        make_ch<EV, NCH, NR>(ctl, rym, hym);
+        make_ch<EV, NCH, NR>(ctl, ryp, hyp);
+        make_ch<EV, NCH, NR>(ctl, rzm, hzm);
+        make_ch<EV, NCH, NR>(ctl, rzp, hzp);
+#pragma unroll
+        for (int h = 0; h < NCH; ++h)
+            nb[c][h] = Nb{hc[h], hxm[h], hxp[h], hym[h], hyp[h], hzm[h], hzp[h]};
+    }
+    Centre<EV, EP, NC, K> z;
+    const double* ctr = pc + NR * NC * RAW3;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        z.fu[c] = FU ? ctr[c * CTR3 + co] : 0.0;
+        if constexpr (EP == EP_LEJA || EP == EP_ARN) {
+            z.y[c] = yc[c];
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                z.p[q][c] = (EP == EP_ARN && q == a.nwin - 1)
+                                ? yc[c] : ctr[((FU + q) * NC + c) * CTR3 + co];
+        }
+    }
+    double val[NC];
+    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
+    epilogue<EV, EP, NC, K>(a, ctl, i * plane + (long)jy * n + kx, val, z, acc);
+}
+
+constexpr int T3 = 512, NW3 = T3 / 32;  // one warp per item row
+
+template <class P, int EV, int EP, int K, int S>
+__global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
+    static_assert(S >= 4, "plane ring needs i-1, i, i+1 and one in flight");
+    constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NR = nraw<EV>();
+    constexpr int SD = stage3_doubles<EV, EP, NC, K>();
+    extern __shared__ __align__(1024) double smem[];
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ int released[S];  // warps that released stage s, cumulative
+
+    Ctl ctl;
+    if (!load_ctl<EV, EP>(a, ctl)) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n = (int)a.g.n, rows = (int)a.g.rows;
+    const long nitems = (long)((n + I3X - 1) / I3X) * ((n + I3Y - 1) / I3Y) *
+                        ((rows + SEG3 - 1) / SEG3);
+    const long G = gridDim.x;
+    const double* rb[2];
+    const double* rh[2];
+    raw_fields<EV>(a, rb, rh);
+
+    // Issue the plane S sequence numbers after position `pos` of item t
+    // (if any) into stage s.
+    auto issue_ahead = [&](long t, Item3 it, int pos, int s) {
+        pos += S;
+        while (pos >= it.L + 2) {
+            pos -= it.L + 2;
+            t += G;
+            if (t >= nitems) return;
+            it = item3(t, n, rows);
+        }
+        issue_plane<EV, EP, NC, K>(a, maps, smem + s * SD, &full[s], it, pos, rows, ctl.active);
+    };
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int t = 0; t < NR + nctr_maps<EV, EP, K>(); ++t)
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&maps.m[t]) : "memory");
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            released[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // fill the ring: sequence numbers 0 .. S-1
+        if (blockIdx.x < nitems) {
+            const Item3 it0 = item3(blockIdx.x, n, rows);
+            for (int s = 0; s < S; ++s) issue_ahead(blockIdx.x, it0, s - S, s);
+        }
+    }
+    __syncthreads();
+
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+
+    auto wait_full = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
+    // This warp is done with sequence number q (position pos of item t). The
+    // last of the NW3 warps to release the stage refills it with the plane S
+    // sequence numbers ahead, so no warp ever waits for another one.
+    auto release = [&](int q, long t, const Item3& it, int pos) {
+        __syncwarp();
+        if (lane == 0) {
+            // the stage's shared-memory reads of this warp have completed
+            // (their values were consumed above), so no fence is needed
+            // before the copy engine may overwrite it
+            const int s = q % S;
+            if ((atomicAdd(&released[s], 1) + 1) % NW3 == 0) issue_ahead(t, it, pos, s);
+        }
+    };
+
+    // this thread's 2 points of a plane: row wid, columns lane + {0, 32}
+    int q0 = 0;  // sequence number of position 0 of the current item
+    for (long t = blockIdx.x; t < nitems; t += G) {
+        const Item3 it = item3(t, n, rows);
+        const bool edge = it.k0 < 1 || it.k0 + I3X >= n || it.j0 < 1 || it.j0 + I3Y >= n;
+        wait_full(q0);
+        wait_full(q0 + 1);
+        int sm = q0 % S, sc = (q0 + 1) % S;
+        for (int p = 1; p <= it.L; ++p) {
+            wait_full(q0 + p + 1);
+            const int sp = sc + 1 == S ? 0 : sc + 1;
+            const double* pm = smem + sm * SD;
+            const double* pc = smem + sc * SD;
+            const double* pp = smem + sp * SD;
+            const long i = it.i0 + p - 1;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ly = wid, lx = lane + 32 * h;
+                const int jy = it.j0 + ly, kx = it.k0 + lx;
+                const int ro = (1 + ly) * TBW3 + 2 + lx, co = ly * I3X + lx;
+                if (!edge)
+                    tma3_point<P, EV, EP, K, false>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co, n,
+                                                    acc);
+                else if (jy < n && kx < n)
+                    tma3_point<P, EV, EP, K, true>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co, n,
+                                                   acc);
+            }
+            release(q0 + p - 1, t, it, p - 1);
+            sm = sc;
+            sc = sp;
+        }
+        release(q0 + it.L, t, it, it.L);
+        release(q0 + it.L + 1, t, it, it.L + 1);
+        q0 += it.L + 2;
+    }
+    reduce_and_finalize<EV, EP, NQ, T3>(a, acc);
+}
+
+}  // namespace ek

@@ -14,6 +14,7 @@
 #include "ek_common.cuh"
 #include "ek_stencil.cuh"
 #include "ek_stream.cuh"
+#include "ek_stream3.cuh"
 #include "ek_vector.cuh"
 
 namespace ek {
@@ -188,7 +189,8 @@ static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 // The TMA-staged kernel needs 16-byte aligned row segments of every field.
 static bool tma_ok(const KArgs& a) {
-    if (a.g.dim != 2 || (a.g.n & 1) || a.g.n < 2 || (a.npts & 1)) return false;
+    if ((a.g.dim != 2 && a.g.dim != 3) || (a.g.n & 1) || a.g.n < 2 || (a.npts & 1)) return false;
+    if (a.g.rows < 1 || a.g.n * a.g.ncomp * a.g.rows >= (int64_t)1 << 31) return false;
     const void* ps[] = {a.u, a.y, a.k, a.fu, a.hu, a.hy, a.hk};
     for (const void* p : ps)
         if (p && !al16(p)) return false;
@@ -204,6 +206,14 @@ template <int EV, int EP, int NC, int K>
 constexpr int tma_stages() {
     constexpr int bytes = stage_doubles<EV, EP, NC, K>() * 8;
     return bytes * 4 <= 110 * 1024 ? 4 : (bytes * 3 <= 110 * 1024 ? 3 : 2);
+}
+// 3-D plane ring: i-1, i, i+1 resident plus S-3 planes in flight; two
+// blocks per SM if that leaves >= 5 stages, else one (0: no TMA variant).
+template <int EV, int EP, int NC, int K>
+constexpr int tma_stages3() {
+    constexpr int bytes = stage3_doubles<EV, EP, NC, K>() * 8;
+    constexpr int two = (110 * 1024) / bytes, one = (220 * 1024) / bytes;
+    return two >= 5 ? (two > 12 ? 12 : two) : (one >= 5 ? (one > 12 ? 12 : one) : 0);
 }
 
 // ---- tensor maps (driver entry point through the runtime, cached)
@@ -222,66 +232,105 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 struct MapEntry {
     const void* p;
-    int64_t cols, rows;
-    uint32_t bw, bh;
+    int rank;
+    int64_t d[3];
+    uint32_t b[3];
     CUtensorMap map;
 };
 
-// (ptr, cols, rows, box) -> encoded map; the Leja / Arnoldi loops reuse a
-// handful of buffers, so the cache turns encoding into a lookup.
-static bool tensor_map(CUtensorMap* out, const double* p, int64_t cols, int64_t rows, uint32_t bw,
-                       uint32_t bh) {
-    static MapEntry cache[64];
+// (ptr, dims, box) -> encoded map of a dense row-major fp64 tensor; the Leja
+// / Arnoldi loops reuse a handful of buffers, so the cache turns encoding
+// into a lookup.
+static bool tensor_map_nd(CUtensorMap* out, const double* p, int rank, const int64_t* d,
+                          const uint32_t* b) {
+    static MapEntry cache[96];
     static int next = 0;
-    for (auto& e : cache)
-        if (e.p == p && e.cols == cols && e.rows == rows && e.bw == bw && e.bh == bh) {
+    for (auto& e : cache) {
+        if (e.p != p || e.rank != rank) continue;
+        bool same = true;
+        for (int r = 0; r < rank; ++r) same = same && e.d[r] == d[r] && e.b[r] == b[r];
+        if (same) {
             *out = e.map;
             return true;
         }
+    }
     auto fn = encode_fn();
     if (!fn) return false;
     MapEntry& e = cache[next];
-    next = (next + 1) % 64;
-    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)cols * 8};
-    const cuuint32_t box[2] = {bw, bh};
-    const cuuint32_t es[2] = {1, 1};
-    if (fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)p, dims, strides, box, es,
+    next = (next + 1) % 96;
+    cuuint64_t dims[3], strides[2];
+    cuuint32_t box[3], es[3];
+    cuuint64_t st = 8;
+    for (int r = 0; r < rank; ++r) {
+        dims[r] = (cuuint64_t)d[r];
+        box[r] = b[r];
+        es[r] = 1;
+        if (r > 0) strides[r - 1] = st;
+        st *= (cuuint64_t)d[r];
+    }
+    if (fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, (void*)p, dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
         e.p = nullptr;
         return false;
     }
     e.p = p;
-    e.cols = cols;
-    e.rows = rows;
-    e.bw = bw;
-    e.bh = bh;
+    e.rank = rank;
+    for (int r = 0; r < 3; ++r) {
+        e.d[r] = r < rank ? d[r] : 0;
+        e.b[r] = r < rank ? b[r] : 0;
+    }
     *out = e.map;
     return true;
+}
+static bool tensor_map(CUtensorMap* out, const double* p, int64_t cols, int64_t rows, uint32_t bw,
+                       uint32_t bh) {
+    const int64_t d[2] = {cols, rows};
+    const uint32_t b[2] = {bw, bh};
+    return tensor_map_nd(out, p, 2, d, b);
+}
+static bool tensor_map3(CUtensorMap* out, const double* p, int64_t n, int64_t planes, uint32_t bw,
+                        uint32_t bh) {
+    const int64_t d[3] = {n, n, planes};
+    const uint32_t b[3] = {bw, bh, 1};
+    return tensor_map_nd(out, p, 3, d, b);
 }
 
 template <int EV, int EP, int NC, int K>
 static bool build_maps(const KArgs& a, TmaMaps& m) {
     memset(&m, 0, sizeof(m));
     const int64_t cols = a.g.n, rt = (int64_t)a.g.ncomp * a.g.rows;
+    const bool d3 = a.g.dim == 3;
+    // 2-D: (ncomp*rows) x n matrix; 3-D: (ncomp*rows) x n x n tensor
+    const uint32_t rw = d3 ? TBW3 : TBW, rh = d3 ? TBR3 : TBR;  // raw boxes
+    const uint32_t cw = d3 ? I3X : 32, ch = d3 ? I3Y : 8;       // centre boxes
+    auto mk = [&](CUtensorMap* out, const double* f, uint32_t bw, uint32_t bh) {
+        return d3 ? tensor_map3(out, f, cols, rt, bw, bh) : tensor_map(out, f, cols, rt, bw, bh);
+    };
     const double* raw[2] = {nullptr, nullptr};
-    if constexpr (EV == EV_RHS) { raw[0] = a.u; }
-    else if constexpr (EV == EV_LIN) { raw[0] = a.y; }
-    else if constexpr (EV == EV_FD || EV == EV_BURGJ) { raw[0] = a.u; raw[1] = a.y; }
-    else { raw[0] = a.k; raw[1] = a.u; }
+    const double* hal[2] = {nullptr, nullptr};
+    if constexpr (EV == EV_RHS) { raw[0] = a.u; hal[0] = a.hu; }
+    else if constexpr (EV == EV_LIN) { raw[0] = a.y; hal[0] = a.hy; }
+    else if constexpr (EV == EV_FD || EV == EV_BURGJ) {
+        raw[0] = a.u; raw[1] = a.y; hal[0] = a.hu; hal[1] = a.hy;
+    } else { raw[0] = a.k; raw[1] = a.u; hal[0] = a.hk; hal[1] = a.hu; }
     int t = 0;
-    for (int f = 0; f < nraw<EV>(); ++f)
-        if (!tensor_map(&m.m[t++], raw[f], cols, rt, TBW, TBR)) return false;
+    for (int f = 0; f < nraw<EV>(); ++f) {
+        if (!mk(&m.m[t++], raw[f], rw, rh)) return false;
+        if (d3 && a.g.slab &&
+            (!hal[f] || !al16(hal[f]) ||
+             !tensor_map3(&m.h[f], hal[f], cols, 2 * (int64_t)a.g.ncomp, rw, rh)))
+            return false;
+    }
     if constexpr (needs_fu<EV>())
-        if (!tensor_map(&m.m[t++], a.fu, cols, rt, 32, 8)) return false;
+        if (!mk(&m.m[t++], a.fu, cw, ch)) return false;
     if constexpr (EP == EP_LEJA)
         for (int q = 0; q < K && q < a.nk; ++q)
-            if (!tensor_map(&m.m[t++], a.p[q], cols, rt, 32, 8)) return false;
+            if (!mk(&m.m[t++], a.p[q], cw, ch)) return false;
     if constexpr (EP == EP_ARN)
         for (int q = 0; q < K && q < a.nwin + a.naug; ++q) {
             const double* f = arn_slot(a, q);
-            if (!al16(f) || !tensor_map(&m.m[t++], f, cols, rt, 32, 8)) return false;
+            if (!al16(f) || !mk(&m.m[t++], f, cw, ch)) return false;
         }
     return true;
 }
@@ -308,6 +357,28 @@ static int launch_k(const KArgs& a, cudaStream_t s) {
             const unsigned grid = (unsigned)(chunks < cap ? chunks : cap);
             kern<<<grid, TPB, SMEM, s>>>(a, maps);
             EK_LAUNCH_CHECK("tma stencil launch");
+            return EK_OK;
+        }
+    }
+    if constexpr (P::DIM == 3) {
+        TmaMaps maps;
+        constexpr int S = tma_stages3<EV, EP, P::NC, K>();
+        if constexpr (S >= 5) if (g_tma_enabled && tma_ok(a) && build_maps<EV, EP, P::NC, K>(a, maps)) {
+            constexpr int SMEM = S * stage3_doubles<EV, EP, P::NC, K>() * 8;
+            static int tocc = 0;
+            auto kern = k_tma3d<P, EV, EP, K, S>;
+            if (tocc == 0) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, T3, SMEM) !=
+                        cudaSuccess || tocc < 1)
+                    tocc = 1;
+            }
+            const int64_t items = ((a.g.n + I3X - 1) / I3X) * ((a.g.n + I3Y - 1) / I3Y) *
+                                  ((a.g.rows + SEG3 - 1) / SEG3);
+            const int64_t cap = (int64_t)sm_count() * tocc;
+            const unsigned grid = (unsigned)(items < cap ? items : cap);
+            kern<<<grid, T3, SMEM, s>>>(a, maps);
+            EK_LAUNCH_CHECK("tma3 stencil launch");
             return EK_OK;
         }
     }

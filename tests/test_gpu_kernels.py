@@ -150,9 +150,14 @@ def test_fused_leja_is_deterministic_and_matches_generic_path():
 @pytest.mark.parametrize("mk", [lambda: ext.brusselator_periodic_problem(n=130),
                                 lambda: ek.make_problem("adr", n=66),
                                 lambda: ext.burgers2d_problem(n=96),
-                                lambda: ek.make_problem("gray_scott", n=64)])
+                                lambda: ek.make_problem("gray_scott", n=64),
+                                lambda: ext.advdiff3d_problem(n=34),
+                                lambda: ext.advdiff3d_problem(n=8),
+                                lambda: ext.advdiff3d_problem(n=66)],
+                         ids=["bruss130", "adr66", "burgers96", "gs64", "ad3d34", "ad3d8",
+                              "ad3d66"])
 def test_tma_and_register_kernels_agree(mk):
-    """The TMA-staged 2-D kernel and the register-staged one agree bit for
+    """The TMA-staged 2-D / 3-D kernels and the register-staged ones agree bit for
     bit on every elementwise pass (RHS, FD/analytic Jv, remainder). Passes
     with a reduction (Leja, power iteration) partition the grid differently,
     so their norms differ in the last bit and the FD quotient amplifies that:

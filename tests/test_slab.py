@@ -97,12 +97,14 @@ def test_gloo_halo_exchange_and_sums():
 
 # ----------------------------------------------------------------- GPU
 
-def _gpu_run(local, n, comm=None):
+def _gpu_run(local, n, comm=None, dim=2):
     """Power iteration + vertical Leja + one EPIRK5P1 step on the periodic
-    Brusselator, on the full grid (comm None) or this rank's slab."""
+    Brusselator (dim 2) or the 3-D advection-diffusion problem (dim 3), on
+    the full grid (comm None) or this rank's slab."""
     import paper_2211_08948_b200 as ek
     from paper_2211_08948_b200 import ext
-    prob = ext.brusselator_periodic_problem(n=n)
+    prob = (ext.brusselator_periodic_problem(n=n) if dim == 2
+            else ext.advdiff3d_problem(n=n))
     if comm is not None:
         prob = S.distribute(prob, comm)
     xi = ek.get_leja_points(400)
@@ -123,10 +125,11 @@ def _gpu_run(local, n, comm=None):
 
 
 @pytest.mark.gpu
-def test_slab_path_p1_bit_identical():
+@pytest.mark.parametrize("dim,n", [(2, 96), (3, 34)])
+def test_slab_path_p1_bit_identical(dim, n):
     from paper_2211_08948_b200 import _device as D
-    a = _gpu_run(0, 96)
-    b = _gpu_run(0, 96, comm=S.SlabComm())
+    a = _gpu_run(0, n, dim=dim)
+    b = _gpu_run(0, n, comm=S.SlabComm(), dim=dim)
     D.COMM = None
     assert (a["iters"], a["freeze"], a["step_iters"], a["charges"]) == \
         (b["iters"], b["freeze"], b["step_iters"], b["charges"])
@@ -135,24 +138,25 @@ def test_slab_path_p1_bit_identical():
         assert np.array_equal(x, y)
 
 
-def _gpu_worker(rank, world, port, n, q):
+def _gpu_worker(rank, world, port, n, q, dim=2):
     _init(rank, world, port)
     try:
         torch.cuda.set_device(0)
-        out = _gpu_run(0, n, comm=S.SlabComm())
+        out = _gpu_run(0, n, comm=S.SlabComm(), dim=dim)
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-def test_two_ranks_match_single_gpu():
-    n = 128
-    ref = _gpu_run(0, n)
+@pytest.mark.parametrize("dim,n", [(2, 128), (3, 34)])
+def test_two_ranks_match_single_gpu(dim, n):
+    ref = _gpu_run(0, n, dim=dim)
     world, port = 2, _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, n, q, dim))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
