@@ -101,7 +101,10 @@ typedef struct ek_leja_state {
     int32_t defer;      /* slab mode: kernels leave their local sums in
                            part[] and ek_leja_decide applies the decision
                            to the rank-ordered global sums                  */
-    int32_t pad_;
+    int32_t p_init;     /* host: -1 requests folding m = 0 into the first
+                           iteration (see ek_leja_begin_len). Device: 1 when
+                           p_i holds d_i[0] b, 0 while the first fused
+                           iteration (m = 1) still has to write it       */
     double part[2];     /* local ||y||^2 and non-finite count                */
 } ek_leja_state;
 
@@ -193,7 +196,12 @@ int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu,
  * m - chunk_base. */
 
 /* m = 0 of leja_interpolate_vertical (leja.py:159-165): p_i = d_i[0]*b,
- * ||b||, freeze test, FD increment for m = 1. */
+ * ||b||, freeze test, FD increment for m = 1. If the host set
+ * st->p_init = -1 (fold request; not in slab mode), this pass only takes
+ * the norm and the decisions: the first ek_leja_run iteration writes
+ * p_i = d_i[0]*b + d_i[1]*y_1 in its own pass (same two roundings), and if
+ * every accumulator froze at m = 0 a follow-up pass on the device writes
+ * p_i = d_i[0]*b. */
 int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
                       const double* coef_dev, ek_leja_state* st, double* work,
                       void* stream);

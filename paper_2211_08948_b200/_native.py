@@ -39,7 +39,7 @@ class LejaState(C.Structure):
                 ("status", C.c_int32), ("k", C.c_int32), ("active", C.c_uint32),
                 ("fd_evals", C.c_int32), ("ticket", C.c_uint32),
                 ("iters", C.c_int32), ("freeze", C.c_int32 * 8), ("defer", C.c_int32),
-                ("pad_", C.c_int32), ("part", C.c_double * 2)]
+                ("p_init", C.c_int32), ("part", C.c_double * 2)]
 
 
 class ScalarState(C.Structure):

@@ -243,6 +243,8 @@ struct Ctl {
     double shift;
     double d[8];
     bool y_zero;          // FD closure shortcut: J 0 = 0 (integrators.py:89-90)
+    bool pinit;           // Leja: accumulators already hold d_i[0] b
+    double d0[8];         // Leja, first iteration: d_i[0]
     double augc[5];       // Arnoldi: tail[aug_tail[t]] * nu (exact: nu = 2^-e)
 };
 
@@ -347,6 +349,7 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     ctl.active = 0u;
     ctl.shift = 0.0;
     ctl.y_zero = false;
+    ctl.pinit = true;
     if constexpr (EP == EP_LEJA) {
         const ek_leja_state* st = (const ek_leja_state*)a.st;
         if (st->done) return false;
@@ -354,8 +357,12 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
         ctl.active = st->active;
         ctl.y_zero = (EV == EV_FD) && (st->ny == 0.0);
         ctl.shift = a.coef[a.mi];
+        ctl.pinit = st->p_init != 0;  // 0 only before the first iteration (m = 1, chunk 0)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) ctl.d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
+        for (int q = 0; q < 8; ++q) {
+            ctl.d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
+            ctl.d0[q] = q < a.nk ? a.coef[(1 + q) * 32] : 0.0;
+        }
     } else if constexpr (EP == EP_POWER) {
         const ek_power_state* st = (const ek_power_state*)a.st;
         if (st->done || st->status) return false;
@@ -387,6 +394,12 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     return true;
 }
 
+// Centre slots a streaming kernel has to fetch (bit q: accumulator /
+// Arnoldi slot q); none of the Leja accumulators before they exist.
+__device__ __forceinline__ uint32_t ctr_mask(const Ctl& ctl) {
+    return ctl.pinit ? ctl.active : 0u;
+}
+
 // EP_ARN centre slot q: window row q (q < nwin), else augmentation q - nwin
 __host__ __device__ __forceinline__ const double* arn_slot(const KArgs& a, int q) {
     return q < a.nwin ? a.win[q] : a.aug[q - a.nwin];
@@ -412,7 +425,7 @@ __device__ __forceinline__ void load_centre(const KArgs& a, const Ctl& ctl, long
             z.y[c] = __ldg(a.y + e);
 #pragma unroll
             for (int q = 0; q < K; ++q)
-                z.p[q][c] = ((ctl.active >> q) & 1u) ? a.p[q][e] : 0.0;
+                z.p[q][c] = (ctl.pinit && ((ctl.active >> q) & 1u)) ? a.p[q][e] : 0.0;
         } else if constexpr (EP == EP_ARN) {
 #pragma unroll
             for (int q = 0; q < K; ++q)
@@ -440,8 +453,15 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
 #pragma unroll
             for (int q = 0; q < K; ++q) {
-                if ((ctl.active >> q) & 1u)
-                    a.p[q][e] = z.p[q][c] + (ctl.d[q] * yn);  // ps[i] + dds[i][m]*y  leja.py:179
+                if (ctl.pinit) {
+                    if ((ctl.active >> q) & 1u)
+                        a.p[q][e] = z.p[q][c] + (ctl.d[q] * yn);  // ps[i] + dds[i][m]*y  leja.py:179
+                } else if (q < a.nk) {
+                    // first iteration with the m = 0 term folded in: ps[i] = dds[i][0]*b
+                    // (leja.py:161), then ps[i] + dds[i][1]*y -- same two roundings
+                    const double p0 = ctl.d0[q] * z.y[c];
+                    a.p[q][e] = ((ctl.active >> q) & 1u) ? p0 + (ctl.d[q] * yn) : p0;
+                }
             }
         } else if constexpr (EP == EP_POWER) {
             a.out[e] = v;
@@ -677,6 +697,7 @@ template <int EV, int EP>
 __device__ void finalize(const KArgs& a, const double* tot) {
     if constexpr (EP == EP_LEJA) {
         ek_leja_state* st = (ek_leja_state*)a.st;
+        st->p_init = 1;
         if (st->defer) {  // slab mode: ek_leja_decide finishes with global sums
             st->part[0] = tot[0];
             st->part[1] = tot[1];

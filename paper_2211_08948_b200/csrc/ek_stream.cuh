@@ -72,13 +72,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+// try_wait with a suspend-time hint: the warp sleeps until the phase
+// completes (or the hint expires) instead of spinning on issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "LAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra LAB_WAIT;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x100000u)
         : "memory");
 }
 
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
                 }
                 const int t = (int)blockIdx.x + issued * G;
                 issue_chunk<EV, EP, NC, K>(maps, smem + s * SD, &full[s], (t % tiles_c) * 32,
-                                           (t / tiles_c) * 8, rows, ctl.active);
+                                           (t / tiles_c) * 8, rows, ctr_mask(ctl));
                 ++issued;
             }
         }

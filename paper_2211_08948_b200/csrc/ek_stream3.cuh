@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
             if (t >= nitems) return;
             it = item3(t, n, rows);
         }
-        issue_plane<EV, EP, NC, K>(a, maps, smem + s * SD, &full[s], it, pos, rows, ctl.active);
+        issue_plane<EV, EP, NC, K>(a, maps, smem + s * SD, &full[s], it, pos, rows, ctr_mask(ctl));
     };
 
     if (threadIdx.x == 0) {

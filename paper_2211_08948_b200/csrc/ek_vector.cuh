@@ -77,6 +77,9 @@ struct LejaVArgs {
 
 // m = 0 of the Newton-Leja sum (leja.py:159-165).
 __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
+    // fold request (host set p_init = -1): leave p to the first iteration.
+    // Every block reads the flag before the last one rewrites it.
+    const bool fold = a.st->p_init < 0;
     double acc[1] = {0.0};
     double d[8];
 #pragma unroll
@@ -85,15 +88,18 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
          e += (int64_t)gridDim.x * TPB) {
         const double y = __ldg(a.b + e);
         acc[0] += y * y;
+        if (!fold) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (q < a.nk) a.p[q][e] = d[q] * y;  // dds[i][0] * y
+            for (int q = 0; q < 8; ++q)
+                if (q < a.nk) a.p[q][e] = d[q] * y;  // dds[i][0] * y
+        }
     }
     block_sum<1>(acc);
     if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
         double tot[1];
         gather_partials<1>(a.work, gridDim.x, tot);
         if (threadIdx.x == 0) {
+            a.st->p_init = fold ? 0 : 1;
             if (a.st->defer) {
                 a.st->part[0] = tot[0];
                 a.st->part[1] = 0.0;
@@ -101,6 +107,22 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
                 leja_begin_decide(a.st, a.coef, a.nk, tot[0]);
             }
         }
+    }
+}
+
+// Folded begin: if every accumulator froze at m = 0 no iteration will write
+// the accumulators, so write p_i = d_i[0] b here (a no-op otherwise).
+__global__ void __launch_bounds__(TPB) k_leja_fold_done(const LejaVArgs a) {
+    if (!a.st->done || a.st->p_init != 0) return;
+    double d[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32] : 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
+         e += (int64_t)gridDim.x * TPB) {
+        const double y = __ldg(a.b + e);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < a.nk) a.p[q][e] = d[q] * y;  // dds[i][0] * y
     }
 }
 

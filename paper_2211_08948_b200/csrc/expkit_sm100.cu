@@ -623,6 +623,10 @@ int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
     for (int q = 0; q < k; ++q) a.p[q] = p[q];
     k_leja_begin<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
     EK_LAUNCH_CHECK("k_leja_begin");
+    // folded begin that froze everything at m = 0: write d_i[0] b (early
+    // exit in every other case)
+    k_leja_fold_done<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
+    EK_LAUNCH_CHECK("k_leja_fold_done");
     return EK_OK;
 }
 

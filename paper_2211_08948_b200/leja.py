@@ -228,7 +228,11 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
 
     slab = Jn is not None and Jn.comm is not None
     ps = [D.empty(n) for _ in range(k)]
-    st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k, defer=1 if slab else 0)
+    # fused single-GPU path: the begin pass only takes ||b|| and the m = 0
+    # decisions; the first iteration writes p_i = d_i[0] b + d_i[1] y_1
+    fold = Jn is not None and not slab and max_points > 1
+    st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k, defer=1 if slab else 0,
+                    p_init=-1 if fold else 0)
     ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(Jn.grid)) if Jn else None)
     pp = N.ptrs(ps)
     N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()), pp, k,
