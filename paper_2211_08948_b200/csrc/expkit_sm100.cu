@@ -233,6 +233,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct MapEntry {
     const void* p;
     int rank;
+    int promo;
     int64_t d[3];
     uint32_t b[3];
     CUtensorMap map;
@@ -241,12 +242,16 @@ struct MapEntry {
 // (ptr, dims, box) -> encoded map of a dense row-major fp64 tensor; the Leja
 // / Arnoldi loops reuse a handful of buffers, so the cache turns encoding
 // into a lookup.
+// L2 promotion: 256-B for boxes whose rows are 256-B aligned (centre
+// fields); none for the neighbourhood boxes, whose rows start 16 B before a
+// 256-B boundary and would otherwise pull three 256-B lines per row.
 static bool tensor_map_nd(CUtensorMap* out, const double* p, int rank, const int64_t* d,
                           const uint32_t* b) {
     static MapEntry cache[96];
     static int next = 0;
+    const int promo = (b[0] % 32 == 0) ? 1 : 0;
     for (auto& e : cache) {
-        if (e.p != p || e.rank != rank) continue;
+        if (e.p != p || e.rank != rank || e.promo != promo) continue;
         bool same = true;
         for (int r = 0; r < rank; ++r) same = same && e.d[r] == d[r] && e.b[r] == b[r];
         if (same) {
@@ -270,12 +275,14 @@ static bool tensor_map_nd(CUtensorMap* out, const double* p, int rank, const int
     }
     if (fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, (void*)p, dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+           promo ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
         e.p = nullptr;
         return false;
     }
     e.p = p;
     e.rank = rank;
+    e.promo = promo;
     for (int r = 0; r < 3; ++r) {
         e.d[r] = r < rank ? d[r] : 0;
         e.b[r] = r < rank ? b[r] : 0;
