@@ -34,6 +34,7 @@ extern "C" {
 #define EK_ERR_INVALID 1      /* bad argument (-> ValueError)                */
 #define EK_ERR_CUDA 2         /* CUDA runtime failure                        */
 #define EK_ERR_UNSUPPORTED 3  /* combination not implemented                 */
+#define EK_ERR_NONFINITE 4    /* non-finite result (-> FloatingPointError)   */
 
 /* device-side numerical status codes (ek_*_state.status) */
 #define EK_ST_OK 0
@@ -323,6 +324,48 @@ int ek_selftest_div(int64_t n, const double* x, const double* d, double* fast,
 /* y = A x, A dense row-major (linalg.py:87-90 from_matrix). */
 int ek_dense_gemv(int64_t n, const double* A, const double* x, double* y,
                   void* stream);
+
+/* -------------------------------------------------------- handle layer */
+/* Context / operator handles over the grid-level entry points, for hosts
+ * that prefer an object API. The library owns the
+ * handles' workspaces and state blocks; vectors stay caller-owned. */
+typedef struct ek_ctx ek_ctx;
+typedef struct ek_op ek_op;
+
+/* Bind a device and the stream every call on this context runs on. NULL on
+ * failure (ek_last_error). Multi-GPU: one context per process/GPU; the
+ * slab exchange itself is the host framework's (torch.distributed / NCCL). */
+ek_ctx* ek_ctx_create(int device, void* stream);
+void ek_ctx_destroy(ek_ctx* ctx);
+
+/* Operator of one problem on one grid (problem id, dims, components, bc,
+ * parameters: all in `g`) with the Jacobian kind jac (EK_JAC_FD /
+ * EK_JAC_ANALYTIC) -- the native counterpart of MatrixFreeOperator over a
+ * Problem's rhs / jac_factory (linalg.py:67-85, problems.py:46-60). */
+ek_op* ek_op_create(ek_ctx* ctx, const ek_grid* g, int jac);
+void ek_op_destroy(ek_op* op);
+
+/* make_linearized (integrators.py:80-96): fu = f(u), *out_norm_u_host =
+ * ||u||; (u, fu) become the operator's linearisation point. Syncs. */
+int ek_op_linearize(ek_op* op, const double* u, double* fu, double* out_norm_u_host);
+/* out = f(u) */
+int ek_op_rhs(ek_op* op, const double* u, double* out);
+/* out = J v at the linearisation point. FD (fd_jacobian_apply,
+ * linalg.py:111-129): eps = (sqrt(eps_mach)*(1+||u||))/||v||; ||v|| = 0 ->
+ * EK_ERR_INVALID, non-finite result -> EK_ERR_NONFINITE. Syncs (FD). */
+int ek_op_jv(ek_op* op, const double* v, double* out);
+/* One power-iteration step (spectrum.py:56-58): w = J v, *norm_out_host =
+ * ||w||. Syncs. */
+int ek_power_step(ek_op* op, const double* v, double* w, double* norm_out_host);
+
+/* out = (a*x) + (b*y), NumPy order. */
+int ek_axpby(int64_t n, double a, const double* x, double b, const double* y,
+             double* out, void* stream);
+/* st->val[i] = x . ys[i] for i < k <= 8, one pass, deterministic block
+ * partials (the window dots of kiops.py:188-190). out_host (nullable):
+ * the k results copied to the host (syncs). work: ek_workspace_bytes. */
+int ek_dot_multi(int64_t n, const double* x, const double* const* ys, int k,
+                 ek_scalar_state* st, double* out_host, double* work, void* stream);
 
 #ifdef __cplusplus
 }

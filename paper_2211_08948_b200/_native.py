@@ -11,7 +11,7 @@ from pathlib import Path
 _HERE = Path(__file__).resolve().parent
 LIB_NAME = "libexpkit_sm100.so"
 
-EK_OK, EK_ERR_INVALID, EK_ERR_CUDA, EK_ERR_UNSUPPORTED = 0, 1, 2, 3
+EK_OK, EK_ERR_INVALID, EK_ERR_CUDA, EK_ERR_UNSUPPORTED, EK_ERR_NONFINITE = 0, 1, 2, 3, 4
 ST_OK, ST_JV_NONFINITE, ST_NORM_NONFINITE, ST_REM_NONFINITE = 0, 1, 2, 3
 
 # enum ek_problem
@@ -110,6 +110,16 @@ _SIGS = {
                         C.POINTER(C.c_int32), C.POINTER(_D), C.POINTER(C.c_int32),
                         C.POINTER(_D), _I, _P, _P, _P]),
     "ek_dense_gemv": (_I, [_L, _P, _P, _P, _P]),
+    "ek_ctx_create": (_P, [_I, _P]),
+    "ek_ctx_destroy": (None, [_P]),
+    "ek_op_create": (_P, [_P, C.POINTER(Grid), _I]),
+    "ek_op_destroy": (None, [_P]),
+    "ek_op_linearize": (_I, [_P, _P, _P, C.POINTER(_D)]),
+    "ek_op_rhs": (_I, [_P, _P, _P]),
+    "ek_op_jv": (_I, [_P, _P, _P]),
+    "ek_power_step": (_I, [_P, _P, _P, C.POINTER(_D)]),
+    "ek_axpby": (_I, [_L, _D, _P, _D, _P, _P, _P]),
+    "ek_dot_multi": (_I, [_L, _P, _PP, _I, _P, C.POINTER(_D), _P, _P]),
 }
 
 _lib = None
@@ -153,6 +163,8 @@ def check(rc, what=""):
     msg = lib().ek_last_error().decode(errors="replace")
     if rc == EK_ERR_INVALID:
         raise ValueError(f"{what}: {msg}")
+    if rc == EK_ERR_NONFINITE:
+        raise FloatingPointError(f"{what}: {msg}")
     raise NativeError(f"{what}: {msg} (status {rc})")
 
 

@@ -126,6 +126,47 @@ __global__ void __launch_bounds__(TPB) k_leja_fold_done(const LejaVArgs a) {
     }
 }
 
+// out = (a*x) + (b*y)
+__global__ void __launch_bounds__(TPB) k_axpby(int64_t n, double a, const double* __restrict__ x,
+                                               double b, const double* __restrict__ y,
+                                               double* __restrict__ out) {
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * TPB)
+        out[e] = (a * __ldg(x + e)) + (b * __ldg(y + e));
+}
+
+struct DotArgs {
+    int64_t n;
+    const double* x;
+    const double* y[8];
+    int k;
+    ek_scalar_state* st;
+    double* work;
+};
+
+// st->val[q] = x . y_q, q < k, one pass over x
+__global__ void __launch_bounds__(TPB) k_dot_multi(const DotArgs a) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.n;
+         e += (int64_t)gridDim.x * TPB) {
+        const double xv = __ldg(a.x + e);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < a.k) acc[q] += xv * __ldg(a.y[q] + e);
+    }
+    block_sum<8>(acc);
+    if (publish_and_arrive<8>(acc, a.work, &a.st->ticket)) {
+        double tot[8];
+        gather_partials<8>(a.work, gridDim.x, tot);
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a.st->val[q] = q < a.k ? tot[q] : 0.0;
+        }
+    }
+}
+
 // Slab mode: apply a deferred Leja decision to the gathered per-rank sums
 // (`g` = [nranks][2] part[] pairs, summed in rank order).
 __global__ void k_leja_decide(ek_leja_state* st, const double* g, int nranks, const double* coef,

@@ -988,4 +988,175 @@ int ek_dense_gemv(int64_t n, const double* A, const double* x, double* y, void* 
     return EK_OK;
 }
 
+
+// ------------------------------------------------------------ handle layer
+
+struct ek_ctx {
+    int device;
+    cudaStream_t stream;
+};
+
+struct ek_op {
+    ek_ctx* ctx;
+    ek_grid g;
+    int jac;
+    double* work;            // device workspace (block partials)
+    ek_scalar_state* st;     // device scalar state
+    const double* u;         // linearisation point (caller-owned)
+    const double* fu;
+    double nu;               // ||u||
+};
+
+ek_ctx* ek_ctx_create(int device, void* stream) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+        set_error("ek_ctx_create: cudaSetDevice(%d) failed", device);
+        return nullptr;
+    }
+    ek_ctx* c = new ek_ctx;
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    return c;
+}
+
+void ek_ctx_destroy(ek_ctx* ctx) { delete ctx; }
+
+ek_op* ek_op_create(ek_ctx* ctx, const ek_grid* g, int jac) {
+    if (!ctx || !grid_ok(g) || (jac != EK_JAC_FD && jac != EK_JAC_ANALYTIC)) {
+        if (ctx && grid_ok(g)) set_error("ek_op_create: jac=%d", jac);
+        return nullptr;
+    }
+    if (jac == EK_JAC_ANALYTIC && jv_ev(g, jac) < 0) {
+        set_error("ek_op_create: problem %d has no analytic Jacobian", g->problem);
+        return nullptr;
+    }
+    ek_op* op = new ek_op{};
+    op->ctx = ctx;
+    op->g = *g;
+    op->jac = jac;
+    if (cudaMalloc(&op->work, ek_workspace_bytes(g)) != cudaSuccess ||
+        cudaMalloc(&op->st, sizeof(ek_scalar_state)) != cudaSuccess ||
+        cudaMemsetAsync(op->st, 0, sizeof(ek_scalar_state), ctx->stream) != cudaSuccess) {
+        set_error("ek_op_create: device allocation failed");
+        cudaFree(op->work);
+        cudaFree(op->st);
+        delete op;
+        return nullptr;
+    }
+    return op;
+}
+
+void ek_op_destroy(ek_op* op) {
+    if (!op) return;
+    cudaStreamSynchronize(op->ctx->stream);
+    cudaFree(op->work);
+    cudaFree(op->st);
+    delete op;
+}
+
+// read the scalar state block back (syncs the operator's stream)
+static int read_state(ek_op* op, ek_scalar_state* h) {
+    if (cudaMemcpyAsync(h, op->st, sizeof(*h), cudaMemcpyDeviceToHost, op->ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(op->ctx->stream) != cudaSuccess) {
+        set_error("ek_op: state read failed: %s", cudaGetErrorString(cudaGetLastError()));
+        return EK_ERR_CUDA;
+    }
+    return EK_OK;
+}
+
+int ek_op_linearize(ek_op* op, const double* u, double* fu, double* out_norm_u_host) {
+    if (!op || !u || !fu) return EK_ERR_INVALID;
+    const int64_t n = ek_grid_len(&op->g);
+    int rc = ek_rhs(&op->g, u, fu, nullptr, op->ctx->stream);
+    if (rc != EK_OK) return rc;
+    rc = ek_norm2(n, u, op->st, 0, op->work, op->ctx->stream);
+    if (rc != EK_OK) return rc;
+    ek_scalar_state h;
+    if ((rc = read_state(op, &h)) != EK_OK) return rc;
+    op->u = u;
+    op->fu = fu;
+    op->nu = h.val[1];
+    if (out_norm_u_host) *out_norm_u_host = op->nu;
+    return EK_OK;
+}
+
+int ek_op_rhs(ek_op* op, const double* u, double* out) {
+    if (!op) return EK_ERR_INVALID;
+    return ek_rhs(&op->g, u, out, nullptr, op->ctx->stream);
+}
+
+int ek_op_jv(ek_op* op, const double* v, double* out) {
+    if (!op || !op->u) {
+        set_error("ek_op_jv: operator not linearised");
+        return EK_ERR_INVALID;
+    }
+    cudaStream_t s = op->ctx->stream;
+    if (op->jac == EK_JAC_ANALYTIC)
+        return ek_jv(&op->g, op->jac, op->u, op->fu, v, 0.0, out, nullptr, op->work, nullptr, s);
+    const int64_t n = ek_grid_len(&op->g);
+    int rc = ek_norm2(n, v, op->st, 0, op->work, s);
+    if (rc != EK_OK) return rc;
+    ek_scalar_state h;
+    if ((rc = read_state(op, &h)) != EK_OK) return rc;
+    const double nv = h.val[1];
+    if (nv == 0.0) {  // linalg.py:121-122
+        set_error("ek_op_jv: cannot form a finite-difference step for a zero vector");
+        return EK_ERR_INVALID;
+    }
+    const double eps = (SQRT_EPS * (1.0 + op->nu)) / nv;  // linalg.py:123-124
+    if (cudaMemsetAsync(&op->st->flag, 0, sizeof(int32_t), s) != cudaSuccess) return EK_ERR_CUDA;
+    rc = ek_jv(&op->g, op->jac, op->u, op->fu, v, eps, out, op->st, op->work, nullptr, s);
+    if (rc != EK_OK) return rc;
+    if ((rc = read_state(op, &h)) != EK_OK) return rc;
+    if (h.flag & 2) {  // linalg.py:127-128
+        set_error("ek_op_jv: non-finite Jacobian action");
+        return EK_ERR_NONFINITE;
+    }
+    return EK_OK;
+}
+
+int ek_power_step(ek_op* op, const double* v, double* w, double* norm_out_host) {
+    int rc = ek_op_jv(op, v, w);
+    if (rc != EK_OK) return rc;
+    rc = ek_norm2(ek_grid_len(&op->g), w, op->st, 0, op->work, op->ctx->stream);
+    if (rc != EK_OK) return rc;
+    ek_scalar_state h;
+    if ((rc = read_state(op, &h)) != EK_OK) return rc;
+    if (norm_out_host) *norm_out_host = h.val[1];
+    return EK_OK;
+}
+
+int ek_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out,
+             void* stream) {
+    if (n < 0 || !x || !y || !out) return EK_ERR_INVALID;
+    if (n == 0) return EK_OK;
+    k_axpby<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(n, a, x, b, y, out);
+    EK_LAUNCH_CHECK("k_axpby");
+    return EK_OK;
+}
+
+int ek_dot_multi(int64_t n, const double* x, const double* const* ys, int k, ek_scalar_state* st,
+                 double* out_host, double* work, void* stream) {
+    if (n < 1 || k < 1 || k > 8 || !x || !ys || !st || !work) {
+        set_error("ek_dot_multi: bad arguments (n=%lld, k=%d)", (long long)n, k);
+        return EK_ERR_INVALID;
+    }
+    DotArgs a{};
+    a.n = n; a.x = x; a.k = k; a.st = st; a.work = work;
+    for (int q = 0; q < k; ++q) a.y[q] = ys[q];
+    cudaStream_t s = (cudaStream_t)stream;
+    k_dot_multi<<<vgrid(n), TPB, 0, s>>>(a);
+    EK_LAUNCH_CHECK("k_dot_multi");
+    if (out_host) {
+        ek_scalar_state h;
+        if (cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            set_error("ek_dot_multi: read back failed");
+            return EK_ERR_CUDA;
+        }
+        for (int q = 0; q < k; ++q) out_host[q] = h.val[q];
+    }
+    return EK_OK;
+}
+
 }  // extern "C"
