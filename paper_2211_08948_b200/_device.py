@@ -19,15 +19,28 @@ F64 = torch.float64
 
 # ---------------------------------------------------------------- device
 
+_READY = False
+
+
 def device():
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2211_08948_b200 needs a CUDA device (B200); "
-                           "there is no CPU fallback")
-    N.lib()
+    global _READY
+    if not _READY:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2211_08948_b200 needs a CUDA device (B200); "
+                               "there is no CPU fallback")
+        N.lib()
+        _READY = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream():
+    """torch's current stream on the current device (raw handle; the fast
+    accessor avoids building a torch.cuda.Stream object per call)."""
+    if _RAW_STREAM is not None:
+        return C.c_void_p(_RAW_STREAM(torch.cuda.current_device()))
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
@@ -106,7 +119,8 @@ class DevState:
     def __init__(self, ctype, **init):
         self.ctype = ctype
         self.size = C.sizeof(ctype)
-        self.buf = torch.zeros(self.size, dtype=torch.uint8, device=device())
+        # fully initialised by the upload below (no fill kernel)
+        self.buf = torch.empty(self.size, dtype=torch.uint8, device=device())
         self.host = ctype()
         for k, v in init.items():
             setattr(self.host, k, v)
