@@ -244,6 +244,7 @@ struct Ctl {
     double d[8];
     bool y_zero;          // FD closure shortcut: J 0 = 0 (integrators.py:89-90)
     bool pinit;           // Leja: accumulators already hold d_i[0] b
+    uint64_t wpol;        // L2 policy of the streamed outputs (evict first)
     double d0[8];         // Leja, first iteration: d_i[0]
     double augc[5];       // Arnoldi: tail[aug_tail[t]] * nu (exact: nu = 2^-e)
 };
@@ -350,6 +351,7 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     ctl.shift = 0.0;
     ctl.y_zero = false;
     ctl.pinit = true;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(ctl.wpol));
     if constexpr (EP == EP_LEJA) {
         const ek_leja_state* st = (const ek_leja_state*)a.st;
         if (st->done) return false;
@@ -434,6 +436,13 @@ __device__ __forceinline__ void load_centre(const KArgs& a, const Ctl& ctl, long
     }
 }
 
+// Store of a streamed output (read again only by the next pass, long after
+// it has left L2): evict-first, so the re-read halo rows stay resident.
+__device__ __forceinline__ void st_stream(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
+                 : "memory");
+}
+
 // Per-point epilogue; acc[] collects this thread's partial reductions.
 template <int EV, int EP, int NC, int K>
 __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long off,
@@ -444,27 +453,28 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
         const long e = c * a.npts + off;
         const double v = val[c];
         if constexpr (EP == EP_STORE) {
-            a.out[e] = v;
+            st_stream(a.out + e, v, ctl.wpol);
         } else if constexpr (EP == EP_LEJA) {
             // y = J.apply(y)/gamma - (c/gamma + xi[m-1]) * y      leja.py:172
             const double yn = dv(v, a.gamma) - (ctl.shift * z.y[c]);
-            a.out[e] = yn;
+            st_stream(a.out + e, yn, ctl.wpol);
             acc[0] += yn * yn;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
 #pragma unroll
             for (int q = 0; q < K; ++q) {
                 if (ctl.pinit) {
-                    if ((ctl.active >> q) & 1u)
-                        a.p[q][e] = z.p[q][c] + (ctl.d[q] * yn);  // ps[i] + dds[i][m]*y  leja.py:179
+                    if ((ctl.active >> q) & 1u)  // ps[i] + dds[i][m]*y  leja.py:179
+                        st_stream(a.p[q] + e, z.p[q][c] + (ctl.d[q] * yn), ctl.wpol);
                 } else if (q < a.nk) {
                     // first iteration with the m = 0 term folded in: ps[i] = dds[i][0]*b
                     // (leja.py:161), then ps[i] + dds[i][1]*y -- same two roundings
                     const double p0 = ctl.d0[q] * z.y[c];
-                    a.p[q][e] = ((ctl.active >> q) & 1u) ? p0 + (ctl.d[q] * yn) : p0;
+                    st_stream(a.p[q] + e, ((ctl.active >> q) & 1u) ? p0 + (ctl.d[q] * yn) : p0,
+                              ctl.wpol);
                 }
             }
         } else if constexpr (EP == EP_POWER) {
-            a.out[e] = v;
+            st_stream(a.out + e, v, ctl.wpol);
             acc[0] += v * v;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
         } else if constexpr (EP == EP_ARN) {
@@ -475,13 +485,13 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             for (int q = 0; q < K; ++q)
                 if (q >= a.nwin && q < a.nwin + a.naug) augv = augv + (ctl.d[q] * z.p[q][c]);
             const double w = (a.dt * v) + augv;
-            a.out[e] = w;
+            st_stream(a.out + e, w, ctl.wpol);
 #pragma unroll
             for (int q = 0; q < (K < 4 ? K : 4); ++q)
                 if (q < a.nwin) acc[q] += z.p[q][c] * w;
             if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
         } else {  // EP_REM
-            a.out[e] = v;
+            st_stream(a.out + e, v, ctl.wpol);
             acc[0] += isfinite(v) ? 0.0 : 1.0;
         }
     }
