@@ -255,8 +255,10 @@ def run_ours(args, rank, world, local):
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None, "traffic": traffic,
-            "kernel": "k_tma2d<PBruss<true>, EV_FD, EP_LEJA, K, 4> (TMA-staged fused FD Jv "
-                      "+ Leja recurrence + K accumulators + ||y||^2 + device freeze test)",
+            "kernel": "k_march2d<PBruss<true>, EV_FD, EP_LEJA, K, S> for k >= 2 accumulators "
+                      "(bulk-copy row march), k_tma2d<.., 1, 4> (TMA 32x8 chunks) for k = 1: "
+                      "fused FD Jv + Leja recurrence + k accumulators + ||y||^2 + device "
+                      "freeze test",
             "bytes_model": "8*N*(4+2*k_active) per launch, N = 2*n^2",
             "launches": kl, "avg_launch_ms": kt / kl * 1e3 if kl else None,
             "share_of_step": kt / elapsed if elapsed else None,

@@ -157,10 +157,14 @@ const char* ek_last_error(void);
 int ek_version(void);
 /* Number of kernels this library has launched (process-wide). */
 long long ek_launch_count(void);
-/* Select the 2-D stencil implementation: 1 (default) = TMA-staged
- * (cp.async.bulk + mbarrier pipeline), 0 = register-staged. Returns the
- * previous setting. Both give bit-identical results. */
-int ek_set_tma(int enabled);
+/* Select the stencil staging of 2-D grids: 3 (default) = auto (bulk-copy
+ * row march k_march2d for Leja passes with k >= 2 accumulators, TMA 32 x 8
+ * chunks k_tma2d otherwise), 2 = row march everywhere, 1 = TMA chunks
+ * everywhere, 0 = register-staged; 3-D grids use the TMA plane march for
+ * any nonzero mode. A negative mode only queries. Returns the previous
+ * setting. All give bit-identical pointwise results (block partial sums of
+ * norms / dots are grouped differently). */
+int ek_set_tma(int mode);
 /* Bytes of device workspace (block partials) any call on this grid needs. */
 int64_t ek_workspace_bytes(const ek_grid* g);
 /* Stream-ordered copies (kind: 1 = host->device, 2 = device->host; a copy

@@ -126,7 +126,8 @@ _lib = None
 
 
 def lib_path():
-    return _HERE / LIB_NAME
+    # EK_LIB_PATH: an alternative build of the same library (tools/ A/B runs)
+    return Path(os.environ["EK_LIB_PATH"]) if os.environ.get("EK_LIB_PATH") else _HERE / LIB_NAME
 
 
 def lib():
@@ -145,6 +146,8 @@ def lib():
         fn = getattr(handle, name)
         fn.restype = res
         fn.argtypes = args
+    if os.environ.get("EK_TMA_MODE"):  # A/B runs of the stencil staging (tools/)
+        handle.ek_set_tma(int(os.environ["EK_TMA_MODE"]))
     _lib = handle
     return _lib
 

@@ -28,8 +28,12 @@
 
 namespace ek {
 
-constexpr int TBW = 36;          // raw box width
-constexpr int TBR = 10;          // raw box rows
+#ifndef EK_EXP_TBW               // (EK_EXP_*: traffic experiments only, wrong results)
+#define EK_EXP_TBW 36
+#define EK_EXP_TBR 10
+#endif
+constexpr int TBW = EK_EXP_TBW;  // raw box width
+constexpr int TBR = EK_EXP_TBR;  // raw box rows
 constexpr int RAW_SLOT = 368;    // doubles per raw box slot (2944 B, 128-B multiple)
 constexpr int CTR_SLOT = 256;    // 8 x 32 doubles
 constexpr int MAX_MAPS = 11;     // 2 raw + f(u) + 8 accumulators
@@ -72,15 +76,18 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-// try_wait with a suspend-time hint: the warp sleeps until the phase
-// completes (or the hint expires) instead of spinning on issue slots.
+// Blocking wait on an mbarrier phase: try_wait without a suspend-time hint
+// (the hardware parks the warp for a bounded window and wakes it when the
+// phase completes). With an explicit hint ptxas emits a NANOSLEEP retry
+// loop, which quantises the wake-up and measured as the top stall of the
+// row-marching kernel.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "LAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra LAB_WAIT;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(0x100000u)
+        "r"(parity)
         : "memory");
 }
 
@@ -161,7 +168,8 @@ __device__ __forceinline__ void issue_chunk(const TmaMaps& maps, double* buf, ui
     for (int f = 0; f < NR; ++f)
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-            tma_load_2d(buf + (f * NC + c) * RAW_SLOT, &maps.m[f], j0 - 2, c * rows + r0 - 1, bar);
+            tma_load_2d(buf + (f * NC + c) * RAW_SLOT, &maps.m[f], j0 - (TBW - 32) / 2,
+                            c * rows + r0 - (TBR - 8) / 2, bar);
     double* ctr = buf + NR * NC * RAW_SLOT;
 #pragma unroll
     for (int g = 0; g < NCM; ++g) {
@@ -273,7 +281,23 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
     const int tiles_c = (cols + 31) / 32;
     const int nchunks = tiles_c * ((rows + 7) / 8);
     const int G = gridDim.x;
+#ifndef EK_EXP_COLMAJOR
     const int my = nchunks > (int)blockIdx.x ? (nchunks - 1 - (int)blockIdx.x) / G + 1 : 0;
+    auto chunk_pos = [&](int k, int& j0, int& r0) {
+        const int t = (int)blockIdx.x + k * G;
+        j0 = (t % tiles_c) * 32;
+        r0 = (t / tiles_c) * 8;
+    };
+#else  // experiment: block b takes a contiguous run of chunks down the strips
+    const int tiles_r = (rows + 7) / 8;
+    const int cb = (int)((long)nchunks * blockIdx.x / G), ce = (int)((long)nchunks * (blockIdx.x + 1) / G);
+    const int my = ce - cb;
+    auto chunk_pos = [&](int k, int& j0, int& r0) {
+        const int t = cb + k;
+        j0 = (t / tiles_r) * 32;
+        r0 = (t % tiles_r) * 8;
+    };
+#endif
     const double* rb[2];
     const double* rh[2];
     raw_fields<EV>(a, rb, rh);
@@ -304,15 +328,16 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
                     if (issued <= k) mbar_wait(&empty[s], par);
                     else if (!mbar_test(&empty[s], par)) break;
                 }
-                const int t = (int)blockIdx.x + issued * G;
-                issue_chunk<EV, EP, NC, K>(maps, smem + s * SD, &full[s], (t % tiles_c) * 32,
-                                           (t / tiles_c) * 8, rows, ctr_mask(ctl));
+                int jj, rr;
+                chunk_pos(issued, jj, rr);
+                issue_chunk<EV, EP, NC, K>(maps, smem + s * SD, &full[s], jj, rr, rows,
+                                           ctr_mask(ctl));
                 ++issued;
             }
         }
         const int s = k % S;
-        const int t = (int)blockIdx.x + k * G;
-        const int j0 = (t % tiles_c) * 32, r0 = (t / tiles_c) * 8;
+        int j0, r0;
+        chunk_pos(k, j0, r0);
         const int i = r0 + wid, j = j0 + lane;
         const double* raw = smem + s * SD;
         const double* ctr = raw + NR * NC * RAW_SLOT;

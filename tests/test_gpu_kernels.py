@@ -148,17 +148,21 @@ def test_fused_leja_is_deterministic_and_matches_generic_path():
 
 
 @pytest.mark.parametrize("mk", [lambda: ext.brusselator_periodic_problem(n=130),
+                                lambda: ext.brusselator_periodic_problem(n=600),
+                                lambda: ek.make_problem("allen_cahn", n=520),
                                 lambda: ek.make_problem("adr", n=66),
                                 lambda: ext.burgers2d_problem(n=96),
                                 lambda: ek.make_problem("gray_scott", n=64),
                                 lambda: ext.advdiff3d_problem(n=34),
                                 lambda: ext.advdiff3d_problem(n=8),
                                 lambda: ext.advdiff3d_problem(n=66)],
-                         ids=["bruss130", "adr66", "burgers96", "gs64", "ad3d34", "ad3d8",
+                         ids=["bruss130", "bruss600", "ac520", "adr66", "burgers96", "gs64", "ad3d34", "ad3d8",
                               "ad3d66"])
 def test_tma_and_register_kernels_agree(mk):
-    """The TMA-staged 2-D / 3-D kernels and the register-staged ones agree bit for
-    bit on every elementwise pass (RHS, FD/analytic Jv, remainder). Passes
+    """The TMA-staged 2-D kernels (row march, 32 x 8 chunks) / 3-D kernel and
+    the register-staged ones agree bit for bit on every elementwise pass (RHS,
+    FD/analytic Jv, remainder); n = 600 / 520 give the row march interior
+    strips (no domain edge) as well as edge strips. Passes
     with a reduction (Leja, power iteration) partition the grid differently,
     so their norms differ in the last bit and the FD quotient amplifies that:
     identical counts, vectors within the FD tier."""
@@ -180,19 +184,23 @@ def test_tma_and_register_kernels_agree(mk):
                                          1e-10, xi=xi)
         return [sys_.f_n, jv, rem], lam, r
 
-    old = N.lib().ek_set_tma(1)
+    res = {}
+    old = N.lib().ek_set_tma(0)
     try:
-        a, la, ra = run()
-        N.lib().ek_set_tma(0)
-        b, lb, rb = run()
+        for mode in (0, 1, 2, 3):
+            N.lib().ek_set_tma(mode)
+            res[mode] = run()
     finally:
         N.lib().ek_set_tma(old)
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y)
-    assert abs(la - lb) <= 1e-12 * abs(lb)
-    assert ra.iters == rb.iters and ra.freeze_iters == rb.freeze_iters
-    for x, y in zip(ra.vectors, rb.vectors):
-        assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y)
+    b, lb, rb = res[0]
+    for mode in (1, 2, 3):
+        a, la, ra = res[mode]
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), mode
+        assert abs(la - lb) <= 1e-12 * abs(lb)
+        assert ra.iters == rb.iters and ra.freeze_iters == rb.freeze_iters
+        for x, y in zip(ra.vectors, rb.vectors):
+            assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y)
 
 
 def test_leja_fd_charges_match_iterations():

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--problem", default="brusselator_periodic")
     ap.add_argument("--no-tma", action="store_true")
+    ap.add_argument("--tma-mode", type=int, default=None,
+                    help="2 row march (default), 1 32x8 chunks, 0 register-staged")
     ap.add_argument("--kiops", action="store_true")
     args = ap.parse_args()
 
@@ -32,6 +34,8 @@ def main():
     from paper_2211_08948_b200 import ext, leja as L, _native as NAT
     if args.no_tma:
         NAT.lib().ek_set_tma(0)
+    if args.tma_mode is not None:
+        NAT.lib().ek_set_tma(args.tma_mode)
 
     prob = ext.make_ext_problem(args.problem, n=args.n)
     rhs = ek.CountingRhs(prob.rhs)
@@ -62,7 +66,8 @@ def main():
     lin = args.problem in ("advdiff2d", "advdiff3d")
     base = 4 if fd else (2 if lin else 3)
     per = 8 * n * (base + 2 * args.k)
-    out = {"problem": args.problem, "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
+    out = {"problem": args.problem, "tma_mode": args.tma_mode,
+           "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
            "ms_per_launch": t / args.iters * 1e3, "bytes_per_launch": per,
            "GBps": per * args.iters / t / 1e9}
     print(json.dumps(out))
