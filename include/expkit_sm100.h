@@ -41,6 +41,7 @@ extern "C" {
 #define EK_ST_JV_NONFINITE 1   /* non-finite FD Jacobian action: linalg.py:127-128 -> FloatingPointError */
 #define EK_ST_NORM_NONFINITE 2 /* non-finite ||y||: leja.py:173-175 -> NonConvergence               */
 #define EK_ST_REM_NONFINITE 3  /* non-finite remainder: integrators.py:107-108 -> FloatingPointError */
+#define EK_ST_PEER_TIMEOUT 4   /* peer mode: a rank's pass flag never arrived (no hang: error)     */
 
 /* ------------------------------------------------------------------ grids */
 enum ek_problem {
@@ -257,6 +258,50 @@ int ek_leja_decide(ek_leja_state* st, const double* gathered, int nranks,
 /* which: 0 = power iteration step, 1 = ||v0||, 2 = ||v|| (FD increment). */
 int ek_power_decide(ek_power_state* st, const double* gathered, int nranks,
                     int fd, int which, void* stream);
+
+/* ------------------------------- slab mode over NVLink peer memory */
+/* Fused compute + exchange for the Leja recurrence: every
+ * rank owns one device "window" that all ranks map (CUDA IPC):
+ *   uint64 flag[8]            flag[r] = e+1 once rank r finished pass e
+ *   double red[2][8][2]       [e & 1][r]: rank r's (||y||^2, non-finite) of pass e
+ *   double halo[2][2][ncomp][rowlen]  [parity][0: row -1, 1: row `rows`]
+ * The fused Leja kernel of pass e stores its boundary rows of y' straight
+ * into the neighbours' halo[(e+1) & 1] (reflect ghosts into its own), and
+ * its last block writes its partial sums into every window's red[e & 1]
+ * and then flag[rank] = e+1 (system-scope fences). A one-warp decide kernel
+ * waits for every rank's flag, sums the partials in rank order and applies
+ * the freeze test: no host round trip, no NCCL call per iteration. */
+typedef struct ek_peer {
+    int32_t world;      /* ranks (<= 8)                                    */
+    int32_t rank;
+    int32_t up;         /* rank owning row -1 of this slab, -1: reflect    */
+    int32_t down;       /* rank owning row `rows`, -1: reflect             */
+    int64_t rowlen;     /* points per row (2-D) / plane (3-D)              */
+    int32_t ncomp;
+    int32_t pad_;
+    double* win[8];     /* every rank's window as mapped in this process   */
+} ek_peer;
+#define EK_PEER_HALO_OFFSET 512  /* bytes: flags (64) + red (256), aligned */
+/* Window size for a slab grid. */
+int64_t ek_peer_window_bytes(const ek_grid* g);
+/* Device allocation (zeroed) plus its CUDA IPC handle (64 bytes out). */
+int ek_ipc_alloc(int64_t bytes, void** dptr, void* handle64);
+/* Map another process's window; ek_ipc_close unmaps, ek_ipc_free frees. */
+int ek_ipc_open(const void* handle64, void** dptr);
+int ek_ipc_close(void* dptr);
+int ek_ipc_free(void* dptr);
+/* Leja iterations m in [m_begin, m_end) in peer mode: pass e = epoch0 +
+ * (m - m_begin) reads the ghost rows of y_{m-1} from `halo_b` ([u, y, k]
+ * halo pointers as for ek_leja_run, y entry used only when m == 1) or from
+ * the own window halo[e & 1], and is followed by the decide kernel. `peer`
+ * is a device copy of the ek_peer struct, `win_local` this rank's window.
+ * st->defer must be 1. */
+int ek_leja_run_peer(const ek_grid* g, int jac, const double* u, const double* fu,
+                     const double* b, double* const* ybuf, double* const* p, int k,
+                     const double* coef_dev, int chunk_base, int m_begin, int m_end,
+                     double gamma, ek_leja_state* st, double* work,
+                     const double* const* halo_b, const ek_peer* peer, double* win_local,
+                     int64_t epoch0, void* stream);
 
 /* --------------------------------------------------- KIOPS (kiops.py) */
 /* V[0] = [src ; tail], beta = ||V[0]||, V[0] /= beta, ||V[0,:n]||

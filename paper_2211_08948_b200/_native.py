@@ -12,7 +12,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_NAME = "libexpkit_sm100.so"
 
 EK_OK, EK_ERR_INVALID, EK_ERR_CUDA, EK_ERR_UNSUPPORTED, EK_ERR_NONFINITE = 0, 1, 2, 3, 4
-ST_OK, ST_JV_NONFINITE, ST_NORM_NONFINITE, ST_REM_NONFINITE = 0, 1, 2, 3
+ST_OK, ST_JV_NONFINITE, ST_NORM_NONFINITE, ST_REM_NONFINITE, ST_PEER_TIMEOUT = 0, 1, 2, 3, 4
 
 # enum ek_problem
 P_ADR, P_ALLEN_CAHN, P_BRUSS_PRINTED, P_BRUSS_STANDARD, P_GRAY_SCOTT, \
@@ -40,6 +40,16 @@ class LejaState(C.Structure):
                 ("fd_evals", C.c_int32), ("ticket", C.c_uint32),
                 ("iters", C.c_int32), ("freeze", C.c_int32 * 8), ("defer", C.c_int32),
                 ("p_init", C.c_int32), ("part", C.c_double * 2)]
+
+
+class Peer(C.Structure):
+    """ek_peer: the window map of a slab decomposition in peer mode."""
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("up", C.c_int32),
+                ("down", C.c_int32), ("rowlen", C.c_int64), ("ncomp", C.c_int32),
+                ("pad_", C.c_int32), ("win", C.c_void_p * 8)]
+
+
+PEER_HALO_OFFSET = 512
 
 
 class ScalarState(C.Structure):
@@ -93,6 +103,13 @@ _SIGS = {
     "ek_power_norm": (_I, [_L, _P, _I, _P, _P, _P]),
     "ek_leja_decide": (_I, [_P, _P, _I, _P, _I, _I, _I, _I, _I, _P]),
     "ek_power_decide": (_I, [_P, _P, _I, _I, _I, _P]),
+    "ek_peer_window_bytes": (_L, [C.POINTER(Grid)]),
+    "ek_ipc_alloc": (_I, [_L, C.POINTER(_P), _P]),
+    "ek_ipc_open": (_I, [_P, C.POINTER(_P)]),
+    "ek_ipc_close": (_I, [_P]),
+    "ek_ipc_free": (_I, [_P]),
+    "ek_leja_run_peer": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
+                              _I, _I, _D, _P, _P, _PP, _P, _P, _L, _P]),
     "ek_arnoldi_init": (_I, [_L, _I, _P, C.POINTER(_D), _P, _P, _P, _P]),
     "ek_arnoldi_run": (_I, [C.POINTER(Grid), _I, _P, _P, _PP, _PP,
                             C.POINTER(_I), _I, _D, _I, _I, _P, _P, _I, _I, _I,

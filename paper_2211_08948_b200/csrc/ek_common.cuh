@@ -72,14 +72,15 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ]) {
 // resets the ticket for the next launch.
 template <int NQ>
 __device__ __forceinline__ bool publish_and_arrive(const double (&v)[NQ], double* work,
-                                                   uint32_t* ticket) {
+                                                   uint32_t* ticket, bool sys = false) {
     __shared__ bool s_last;
     const int t = flat_tid();
     if (t == 0) {
         const long b = flat_bid();
 #pragma unroll
         for (int q = 0; q < NQ; ++q) work[b * NQ + q] = v[q];
-        __threadfence();
+        if (sys) __threadfence_system();  // orders the block's peer stores too
+        else __threadfence();
         const uint32_t got = atomicAdd(ticket, 1u);
         s_last = (got == (uint32_t)(nblocks() - 1));
         if (s_last) *ticket = 0u;

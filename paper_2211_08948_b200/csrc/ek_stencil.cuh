@@ -211,6 +211,10 @@ struct KArgs {
     double aug_scale;     // nu (power of two)
     double* H;
     int ldh;
+    // slab mode over peer memory (ek_leja_run_peer): window map and pass
+    // number; null off that mode
+    const ek_peer* peer;
+    long epoch;
 };
 
 // ----------------------------------------------------------------- geometry
@@ -247,7 +251,21 @@ struct Ctl {
     uint64_t wpol;        // L2 policy of the streamed outputs (evict first)
     double d0[8];         // Leja, first iteration: d_i[0]
     double augc[5];       // Arnoldi: tail[aug_tail[t]] * nu (exact: nu = 2^-e)
+    // peer mode: where this pass's boundary rows of y' go ([ncomp][rowlen]
+    // halo slots in a window): row 0 -> up's row `rows` ghost, row rows-1 ->
+    // down's row -1 ghost; at a reflect edge rows 1 / rows-2 -> own ghosts
+    double* h_first;
+    double* h_second;
+    double* h_penult;
+    double* h_last;
+    long rowlen;
 };
+
+// Halo slot [ncomp][rowlen] of (rank r, parity, side) in the peer windows.
+__device__ __forceinline__ double* peer_halo(const ek_peer* P, int r, int parity, int side) {
+    return (double*)((char*)P->win[r] + EK_PEER_HALO_OFFSET) +
+           (long)((parity * 2 + side) * P->ncomp) * P->rowlen;
+}
 
 // Channel values of one grid point.
 template <int EV, int NCH>
@@ -392,8 +410,41 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
                            ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
         }
     }
+    ctl.h_first = ctl.h_second = ctl.h_penult = ctl.h_last = nullptr;
+    ctl.rowlen = 0;
+    if constexpr (EP == EP_LEJA) {
+        if (a.peer) {
+            const ek_peer* P = a.peer;
+            const int par = (int)((a.epoch + 1) & 1);  // read by pass epoch + 1
+            ctl.rowlen = P->rowlen;
+            if (P->up >= 0) ctl.h_first = peer_halo(P, P->up, par, 1);
+            else ctl.h_second = peer_halo(P, P->rank, par, 0);
+            if (P->down >= 0) ctl.h_last = peer_halo(P, P->down, par, 0);
+            else ctl.h_penult = peer_halo(P, P->rank, par, 1);
+        }
+    }
     ctl.eps_d = mkdv(ctl.eps);
     return true;
+}
+
+// Peer mode: copy y'(off) of component c into the halo slots it feeds.
+__device__ __forceinline__ void peer_halo_store(const KArgs& a, const Ctl& ctl, long off, int c,
+                                                double v) {
+    const long rl = ctl.rowlen, lo2 = (a.g.rows - 2) * rl, co = c * rl;
+    if (off < 2 * rl) {
+        if (off < rl) {
+            if (ctl.h_first) ctl.h_first[co + off] = v;
+        } else if (ctl.h_second) {
+            ctl.h_second[co + off - rl] = v;
+        }
+    }
+    if (off >= lo2) {
+        if (off >= lo2 + rl) {
+            if (ctl.h_last) ctl.h_last[co + off - lo2 - rl] = v;
+        } else if (ctl.h_penult) {
+            ctl.h_penult[co + off - lo2] = v;
+        }
+    }
 }
 
 // Centre slots a streaming kernel has to fetch (bit q: accumulator /
@@ -458,6 +509,7 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             // y = J.apply(y)/gamma - (c/gamma + xi[m-1]) * y      leja.py:172
             const double yn = dv(v, a.gamma) - (ctl.shift * z.y[c]);
             st_stream(a.out + e, yn, ctl.wpol);
+            if (ctl.rowlen) peer_halo_store(a, ctl, off, c, yn);
             acc[0] += yn * yn;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
 #pragma unroll
@@ -513,7 +565,9 @@ template <int EV, int EP, int NQ, int NT = TPB>
 __device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc)[NQ]) {
     if constexpr (ep_nq(EP) > 0) {
         block_sum<NQ, NT / 32>(acc);
-        if (publish_and_arrive<NQ>(acc, a.work, ticket_of<EP>(a))) {
+        // peer mode: this block's halo stores must reach the peers before
+        // the last block raises the pass flag (system-scope fence)
+        if (publish_and_arrive<NQ>(acc, a.work, ticket_of<EP>(a), a.peer != nullptr)) {
             double tot[NQ];
             gather_partials<NQ, NT>(a.work, nblocks(), tot);
             if (flat_tid() == 0) finalize<EV, EP>(a, tot);
@@ -708,6 +762,23 @@ __device__ void finalize(const KArgs& a, const double* tot) {
     if constexpr (EP == EP_LEJA) {
         ek_leja_state* st = (ek_leja_state*)a.st;
         st->p_init = 1;
+        if (a.peer) {  // peer mode: partials into every window, then the flag
+            const ek_peer* P = a.peer;
+            const int par = (int)(a.epoch & 1);
+            for (int r = 0; r < P->world; ++r) {
+                double* red = (double*)((char*)P->win[r] + 64) + (par * 8 + P->rank) * 2;
+                red[0] = tot[0];
+                red[1] = tot[1];
+            }
+            __threadfence_system();
+            for (int r = 0; r < P->world; ++r) {
+                unsigned long long* f = (unsigned long long*)P->win[r] + P->rank;
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f),
+                             "l"((unsigned long long)(a.epoch + 1))
+                             : "memory");
+            }
+            return;
+        }
         if (st->defer) {  // slab mode: ek_leja_decide finishes with global sums
             st->part[0] = tot[0];
             st->part[1] = tot[1];

@@ -179,6 +179,45 @@ __global__ void k_leja_decide(ek_leja_state* st, const double* g, int nranks, co
     else leja_decide(st, coef, mi, m, nk, s0, s1, fd != 0);
 }
 
+// Peer mode: wait until every rank raised its flag for pass `epoch`
+// (ld.acquire.sys on the own window), then the rank-ordered sums of the
+// partials the ranks wrote into red[epoch & 1] and the freeze test. A flag
+// that never comes (a dead peer) ends in EK_ST_PEER_TIMEOUT, not a hang.
+__global__ void k_peer_decide(ek_leja_state* st, const ek_peer* P, long epoch, const double* coef,
+                              int mi, int m, int nk, int fd) {
+    if (st->done) return;
+    const int lane = threadIdx.x;
+    const double* win = P->win[P->rank];
+    bool ok = true;
+    if (lane < P->world) {
+        const unsigned long long* f = (const unsigned long long*)win + lane;
+        const unsigned long long want = (unsigned long long)epoch + 1;
+        unsigned long long got = 0, t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(got) : "l"(f) : "memory");
+            if (got >= want) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 60ull * 1000000000ull) {  // 60 s: give up instead of hanging
+                ok = false;
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (lane != 0) return;
+    if (!ok) {
+        st->status = EK_ST_PEER_TIMEOUT;
+        st->done = 1;
+        st->iters = m;
+        return;
+    }
+    double s0, s1;
+    gathered_sums((const double*)((const char*)win + 64) + (epoch & 1) * 16, P->world, s0, s1);
+    leja_decide(st, coef, mi, m, nk, s0, s1, fd != 0);
+}
+
 // Slab mode: deferred power-iteration decision; which = 0 iteration,
 // 1 = ||v0|| (first divisor), 2 = ||v|| (FD increment).
 __global__ void k_power_decide(ek_power_state* st, const double* g, int nranks, int fd,

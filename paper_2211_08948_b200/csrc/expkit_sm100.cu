@@ -432,6 +432,88 @@ int ek_power_decide(ek_power_state* st, const double* gathered, int nranks, int 
     return EK_OK;
 }
 
+// --------------------------------------- slab mode over NVLink peer memory
+int64_t ek_peer_window_bytes(const ek_grid* g) {
+    if (!grid_ok(g) || g->dim < 2) return 0;
+    const int64_t rowlen = g->dim == 2 ? g->n : g->n * g->n;
+    return EK_PEER_HALO_OFFSET + 2 * 2 * (int64_t)g->ncomp * rowlen * (int64_t)sizeof(double);
+}
+
+int ek_ipc_alloc(int64_t bytes, void** dptr, void* handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    if (bytes <= 0 || !dptr || !handle64) {
+        set_error("ek_ipc_alloc: bad arguments");
+        return EK_ERR_INVALID;
+    }
+    cudaError_t e = cudaMalloc(dptr, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaMemset(*dptr, 0, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle((cudaIpcMemHandle_t*)handle64, *dptr);
+    if (e != cudaSuccess) return cuda_status(e, "ek_ipc_alloc");
+    return EK_OK;
+}
+
+int ek_ipc_open(const void* handle64, void** dptr) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_status(e, "ek_ipc_open");
+    return EK_OK;
+}
+
+int ek_ipc_close(void* dptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(dptr);
+    if (e != cudaSuccess) return cuda_status(e, "ek_ipc_close");
+    return EK_OK;
+}
+
+int ek_ipc_free(void* dptr) {
+    cudaError_t e = cudaFree(dptr);
+    if (e != cudaSuccess) return cuda_status(e, "ek_ipc_free");
+    return EK_OK;
+}
+
+int ek_leja_run_peer(const ek_grid* g, int jac, const double* u, const double* fu,
+                     const double* b, double* const* ybuf, double* const* p, int k,
+                     const double* coef_dev, int chunk_base, int m_begin, int m_end,
+                     double gamma, ek_leja_state* st, double* work,
+                     const double* const* halo_b, const ek_peer* peer, double* win_local,
+                     int64_t epoch0, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (k < 1 || k > 8 || !peer || !win_local || !halo_b || !g->slab || g->rows < 2 ||
+        g->dim < 2) {
+        set_error("ek_leja_run_peer: needs a slab grid (rows >= 2), halos, a peer map, 1 <= k <= 8");
+        return EK_ERR_INVALID;
+    }
+    const int ev = jv_ev(g, jac);
+    if (ev < 0) return EK_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t rowlen = g->dim == 2 ? g->n : g->n * g->n;
+    KArgs a;
+    base_args(a, g, halo_b);
+    a.u = u; a.fu = fu; a.nk = k; a.coef = coef_dev; a.gamma = mkdv(gamma); a.st = st; a.work = work;
+    a.peer = peer;
+    for (int q = 0; q < k; ++q) a.p[q] = p[q];
+    for (int m = m_begin; m < m_end; ++m) {
+        const int64_t e = epoch0 + (m - m_begin);
+        a.m = m;
+        a.mi = m - chunk_base;
+        a.epoch = (long)e;
+        a.y = (m == 1) ? b : ybuf[(m - 1) & 1];
+        a.out = ybuf[m & 1];
+        // ghost rows of y_{m-1}: exchanged once for b, else written into the
+        // own window by the neighbours' previous pass
+        a.hy = (m == 1) ? halo_b[1]
+                        : (const double*)((const char*)win_local + EK_PEER_HALO_OFFSET) +
+                              (e & 1) * 2 * (int64_t)g->ncomp * rowlen;
+        const int rc = launch_stencil<EP_LEJA>(ev, a, s);
+        if (rc != EK_OK) return rc;
+        k_peer_decide<<<1, 32, 0, s>>>(st, peer, (long)e, coef_dev, m - chunk_base, m, k,
+                                       jac == EK_JAC_FD ? 1 : 0);
+        EK_LAUNCH_CHECK("k_peer_decide");
+    }
+    return EK_OK;
+}
+
 // ------------------------------------------------------------------ KIOPS
 int ek_arnoldi_init(int64_t n, int p, const double* src, const double* tail_host, double* V0,
                     ek_arnoldi_state* st, double* work, void* stream) {

@@ -272,7 +272,18 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                 import torch
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
-            if slab:
+            if slab and Jn.comm.peer:
+                # peer mode: ghost rows of b once (NCCL), then every pass
+                # stores its boundary rows into the neighbours' windows and
+                # a decide kernel waits for the pass flags: no host work
+                win = Jn.comm.window(Jn.grid)
+                N.check(N.lib().ek_leja_run_peer(
+                    C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
+                    C.c_void_p(Jn.fu.data_ptr()), C.c_void_p(bd.data_ptr()), yp, pp, k,
+                    C.c_void_p(table.dev.data_ptr()), base, m, hi, float(gamma), st.ptr, ws,
+                    Jn.halos(v=bd) if m == 1 else Jn.halos(), win.ptr,
+                    C.c_void_p(win.local), win.take(hi - m), D.stream()), "ek_leja_run_peer")
+            elif slab:
                 # per iteration: ghost rows of y_{m-1}, local fused pass,
                 # all-gather of the local sums, device decision (all ranks
                 # reach the same one, so they stay in lockstep)
@@ -316,6 +327,8 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             raise FloatingPointError("non-finite Jacobian action")
         if hst.status == N.ST_NORM_NONFINITE:
             raise NonConvergence("polynomial iteration diverged", iters=int(hst.iters))
+        if hst.status == N.ST_PEER_TIMEOUT:
+            raise RuntimeError("peer mode: a rank's pass flag did not arrive (dead peer?)")
         if hst.done:
             return LejaResult(vectors=[D.like_input(p, b) for p in ps],
                               iters=int(hst.iters),

@@ -18,6 +18,15 @@ block (`defer`), the ranks all-gather them, and the device decision sums
 them in rank order — identical on every rank, so all ranks take the same
 branch every iteration without any host round trip.
 
+Peer mode (`SlabComm(peer=True)`, the default over NCCL): the Leja
+recurrence — the hot loop — exchanges nothing through NCCL. Every rank maps
+every rank's device window (CUDA IPC over NVLink, `PeerWindow`); the fused
+Leja kernel stores its boundary rows of y' straight into the neighbours'
+halo slots and its partial sums plus a pass flag into every window, and a
+one-warp decide kernel waits for the flags and applies the freeze test
+(`ek_leja_run_peer`). A launch batch of iterations is enqueued like the
+single-GPU one, with no host round trip or NCCL call per iteration.
+
 Activate with `distribute(problem)`; the returned Problem carries a local
 `StencilRhs` and the rank's slice of the initial condition.
 """
@@ -34,9 +43,13 @@ from .problems import NativeJacFactory, Problem, StencilRhs
 
 
 class SlabComm:
-    """Neighbour exchange and rank-ordered sums for one slab decomposition."""
+    """Neighbour exchange and rank-ordered sums for one slab decomposition.
 
-    def __init__(self, group=None):
+    peer: None = on over NCCL (device ranks), off over gloo / single process;
+    True forces it (a single process then maps its own window: the test of
+    the fused path on one GPU), False disables it."""
+
+    def __init__(self, group=None, peer=None):
         if dist.is_available() and dist.is_initialized():
             self.group = group
             self.rank = dist.get_rank(group)
@@ -44,6 +57,19 @@ class SlabComm:
             self.backend = dist.get_backend(group)
         else:
             self.group, self.rank, self.world, self.backend = None, 0, 1, None
+        if peer is None:
+            peer = self.backend == "nccl" and self.world > 1
+        self.peer = bool(peer) and not self.host_staged
+        self._windows = {}
+
+    def window(self, grid):
+        """The PeerWindow of a local slab grid (created collectively on first
+        use; every rank reaches it in the same order)."""
+        key = (int(grid.dim), int(grid.ncomp), int(grid.n), int(grid.rows))
+        w = self._windows.get(key)
+        if w is None:
+            w = self._windows[key] = PeerWindow(self, grid)
+        return w
 
     @property
     def host_staged(self):
@@ -175,6 +201,61 @@ class SlabComm:
         dist.all_gather(bufs, loc, group=self.group)
         parts = [b.cpu().numpy().reshape(ncomp, -1, rowlen) for b in bufs]
         return np.concatenate(parts, axis=1).reshape(-1)
+
+
+class PeerWindow:
+    """This rank's device window and the map of every rank's window
+    (ek_peer, include/expkit_sm100.h): flags, partial sums, halo slots."""
+
+    def __init__(self, comm, grid):
+        lib = N.lib()
+        rows = int(grid.rows)
+        if rows < 2:
+            raise ValueError("peer mode needs slabs of at least two rows")
+        nbytes = lib.ek_peer_window_bytes(C.byref(grid))
+        ptr = C.c_void_p()
+        handle = (C.c_char * 64)()
+        N.check(lib.ek_ipc_alloc(nbytes, C.byref(ptr), handle), "ek_ipc_alloc")
+        self.local = ptr.value
+        mine = bytes(handle)
+        if comm.world > 1:
+            handles = [None] * comm.world
+            dist.all_gather_object(handles, mine, group=comm.group)
+        else:
+            handles = [mine]
+        self._opened = []
+        wins = []
+        for r, h in enumerate(handles):
+            if r == comm.rank:
+                wins.append(self.local)
+            else:
+                p = C.c_void_p()
+                N.check(lib.ek_ipc_open(h, C.byref(p)), "ek_ipc_open")
+                self._opened.append(p.value)
+                wins.append(p.value)
+        periodic = grid.bc == N.BC_PERIODIC
+        up = comm.rank - 1 if comm.rank > 0 else (comm.world - 1 if periodic else -1)
+        down = comm.rank + 1 if comm.rank < comm.world - 1 else (0 if periodic else -1)
+        host = N.Peer(world=comm.world, rank=comm.rank, up=up, down=down,
+                      rowlen=int(grid.n) if grid.dim == 2 else int(grid.n) ** 2,
+                      ncomp=int(grid.ncomp))
+        for r, w in enumerate(wins):
+            host.win[r] = w
+        raw = bytes(host)
+        self.dev = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(D.device())
+        self.epoch = 0  # passes issued so far (identical on every rank)
+        if comm.world > 1:
+            dist.barrier(group=comm.group)
+
+    @property
+    def ptr(self):
+        return C.c_void_p(self.dev.data_ptr())
+
+    def take(self, passes):
+        """Epoch of the first of `passes` consecutive fused passes."""
+        e = self.epoch
+        self.epoch += passes
+        return e
 
 
 def slab_grid(grid, comm):

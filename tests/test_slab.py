@@ -97,14 +97,17 @@ def test_gloo_halo_exchange_and_sums():
 
 # ----------------------------------------------------------------- GPU
 
-def _gpu_run(local, n, comm=None, dim=2):
+def _gpu_run(local, n, comm=None, dim=2, name=None):
     """Power iteration + vertical Leja + one EPIRK5P1 step on the periodic
     Brusselator (dim 2) or the 3-D advection-diffusion problem (dim 3), on
     the full grid (comm None) or this rank's slab."""
     import paper_2211_08948_b200 as ek
     from paper_2211_08948_b200 import ext
-    prob = (ext.brusselator_periodic_problem(n=n) if dim == 2
-            else ext.advdiff3d_problem(n=n))
+    if name == "allen_cahn":  # Neumann (reflect) edges, FD Jacobian
+        prob = ek.make_problem("allen_cahn", n=n)
+    else:
+        prob = (ext.brusselator_periodic_problem(n=n) if dim == 2
+                else ext.advdiff3d_problem(n=n))
     if comm is not None:
         prob = S.distribute(prob, comm)
     xi = ek.get_leja_points(400)
@@ -131,6 +134,29 @@ def test_slab_path_p1_bit_identical(dim, n):
     a = _gpu_run(0, n, dim=dim)
     b = _gpu_run(0, n, comm=S.SlabComm(), dim=dim)
     D.COMM = None
+    assert (a["iters"], a["freeze"], a["step_iters"], a["charges"]) == \
+        (b["iters"], b["freeze"], b["step_iters"], b["charges"])
+    assert a["lam"] == b["lam"] and a["err"] == b["err"]
+    for x, y in zip(a["vecs"], b["vecs"]):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,n,name", [(2, 96, None), (2, 600, None), (2, 64, "allen_cahn"),
+                                        (3, 34, None)])
+def test_peer_mode_p1_bit_identical(dim, n, name):
+    """The fused compute + exchange path (boundary rows stored into the
+    window halo slots by the Leja kernel, pass flags + device decide, no
+    NCCL per iteration), run by one process on its own window (periodic: the
+    rank is its own neighbour; reflect: it writes its own mirror ghosts):
+    bit-identical to the whole-grid path, counts included."""
+    from paper_2211_08948_b200 import _device as D
+    a = _gpu_run(0, n, dim=dim, name=name)
+    comm = S.SlabComm(peer=True)
+    assert comm.peer
+    b = _gpu_run(0, n, comm=comm, dim=dim, name=name)
+    D.COMM = None
+    assert comm._windows and next(iter(comm._windows.values())).epoch > 0  # peer path ran
     assert (a["iters"], a["freeze"], a["step_iters"], a["charges"]) == \
         (b["iters"], b["freeze"], b["step_iters"], b["charges"])
     assert a["lam"] == b["lam"] and a["err"] == b["err"]
