@@ -149,15 +149,18 @@ class ClockSampler:
 
 def leja_bytes(prof):
     """Algorithmic bytes of every fused Leja launch of one call: iteration m
-    reads u, y, f(u) and the k_active accumulators and writes y' and them:
-    8 N (4 + 2 k_active(m)) with FD."""
+    reads u, y and the k_active accumulators and writes y' and them:
+    8 N (3 + 2 k_active(m)) with FD. SURVEY.md §8(d) d3 counts a read of
+    f(u_n) too (8 N (4 + 2k)); the kernel re-evaluates f(u_n) from the u
+    neighbourhood it reads anyway, so that vector is not algorithmic
+    traffic of this implementation."""
     n = prof["n"]
     per_vec = 8 * n
     total, launches = 0, 0
     freeze = prof.get("freeze", [])
     for m in range(1, prof.get("iters", 0) + 1):
         k_act = sum(1 for f in freeze if f >= m)
-        base = 4 if prof["fd"] else 2
+        base = 3 if prof["fd"] else 2
         total += per_vec * (base + 2 * k_act)
         launches += 1
     return total, launches
@@ -255,11 +258,12 @@ def run_ours(args, rank, world, local):
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None, "traffic": traffic,
-            "kernel": "k_march2d<PBruss<true>, EV_FD, EP_LEJA, K, S> for k >= 2 accumulators "
-                      "(bulk-copy row march), k_tma2d<.., 1, 4> (TMA 32x8 chunks) for k = 1: "
+            "kernel": "k_march2d<PBruss<true>, EV_FD, EP_LEJA, K, S> for k >= 3 accumulators "
+                      "(bulk-copy row march), k_tma2d<.., K, 4> (TMA 32x8 chunks) for k <= 2: "
                       "fused FD Jv + Leja recurrence + k accumulators + ||y||^2 + device "
                       "freeze test",
-            "bytes_model": "8*N*(4+2*k_active) per launch, N = 2*n^2",
+            "bytes_model": "8*N*(3+2*k_active) per launch (reads u, y, p_1..k; writes y', "
+                           "p_1..k; f(u_n) is re-evaluated in-kernel, not read), N = 2*n^2",
             "launches": kl, "avg_launch_ms": kt / kl * 1e3 if kl else None,
             "share_of_step": kt / elapsed if elapsed else None,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}

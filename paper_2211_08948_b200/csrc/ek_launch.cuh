@@ -248,10 +248,10 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
     if constexpr (P::DIM == 2) {
         TmaMaps maps;
         // auto (3): the row march where it measured faster on the B200 (Leja
-        // with k >= 2 accumulators: 0.395 vs 0.429 ms at k = 2, 0.439 vs
-        // 0.525 ms at k = 3, config 4), 32 x 8 chunks otherwise (k = 1:
-        // 0.273 vs 0.353 ms)
-        const bool march = g_tma_mode == 2 || (g_tma_mode == 3 && EP == EP_LEJA && K >= 2);
+        // with k >= 3 accumulators: 0.436 vs 0.498 ms at k = 3, config 4),
+        // 32 x 8 chunks otherwise (k = 2: 0.340 vs 0.392 ms, k = 1: 0.252
+        // vs 0.347 ms)
+        const bool march = g_tma_mode == 2 || (g_tma_mode == 3 && EP == EP_LEJA && K >= 3);
         if (march && march_ok(a)) {
             constexpr int S = tma_stages2<EV, EP, P::NC, K>();
             constexpr int SMEM = S * stage2_doubles<EV, EP, P::NC, K>() * 8;

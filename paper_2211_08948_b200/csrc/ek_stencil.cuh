@@ -47,8 +47,13 @@ namespace ek {
 enum { EV_RHS = 0, EV_FD, EV_LIN, EV_BURGJ, EV_REMFD, EV_REMLIN, EV_REMBURG };
 enum { EP_STORE = 0, EP_LEJA, EP_POWER, EP_ARN, EP_REM };
 
+// Channels per point. EV_FD / EV_REMFD carry u itself as the last channel:
+// f(u_n) is re-evaluated from the u neighbourhood the pass reads anyway
+// (same code and order as the RHS pass that produced f_n, so the same bits)
+// instead of streaming f_n from HBM — one vector less per pass.
 __host__ __device__ constexpr int ev_nch(int ev) {
-    return ev == EV_BURGJ ? 2 : ev == EV_REMFD ? 2 : ev == EV_REMLIN ? 2 : ev == EV_REMBURG ? 3 : 1;
+    return ev == EV_FD ? 2 : ev == EV_BURGJ ? 2 : ev == EV_REMFD ? 3 : ev == EV_REMLIN ? 2
+         : ev == EV_REMBURG ? 3 : 1;
 }
 __host__ __device__ constexpr int ep_nq(int ep) {
     return ep == EP_LEJA ? 2 : ep == EP_POWER ? 2 : ep == EP_ARN ? 5 : ep == EP_REM ? 1 : 0;
@@ -276,7 +281,9 @@ __device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const do
     } else if constexpr (EV == EV_FD) {
         double yv = __ldg(py + e);
         if (ctl.has_div) yv = dv(yv, ctl.ydiv);
-        ch[0] = __ldg(pu + e) + ctl.eps * yv;  // u + eps*v   (linalg.py:126)
+        const double uv = __ldg(pu + e);
+        ch[0] = uv + ctl.eps * yv;  // u + eps*v   (linalg.py:126)
+        ch[1] = uv;
     } else if constexpr (EV == EV_LIN) {
         double yv = __ldg(py + e);
         if (ctl.has_div) yv = dv(yv, ctl.ydiv);
@@ -291,6 +298,7 @@ __device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const do
         const double dk = kv - uv;               // dk = k - u_n (integrators.py:103)
         ch[0] = kv;
         ch[1] = uv + ctl.eps * dk;
+        ch[2] = uv;
     } else if constexpr (EV == EV_REMLIN) {
         const double kv = __ldg(pk + e), uv = __ldg(pu + e);
         ch[0] = kv;
@@ -315,26 +323,28 @@ __device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
         for (int c = 0; c < NC; ++c) s[c] = nb[c][0];
         P::f(s, val, a.pc);
     } else if constexpr (EV == EV_FD) {
-        Nb s[NC];
+        Nb s[NC], su[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) s[c] = nb[c][0];
-        double fw[NC];
+        for (int c = 0; c < NC; ++c) { s[c] = nb[c][0]; su[c] = nb[c][1]; }
+        double fw[NC], fu[NC];
         P::f(s, fw, a.pc);
+        P::f(su, fu, a.pc);  // f(u_n), bit-identical to the RHS pass
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-            val[c] = ctl.y_zero ? 0.0 : dv(fw[c] - fuc[c], ctl.eps_d);  // linalg.py:126
+            val[c] = ctl.y_zero ? 0.0 : dv(fw[c] - fu[c], ctl.eps_d);  // linalg.py:126
     } else if constexpr (EV == EV_BURGJ) {
         if constexpr (NC == 1 && NCH == 2) val[0] = PBurgers::jac(nb[0][0], nb[0][1], a.pc);
     } else if constexpr (EV == EV_REMFD) {
-        Nb s0[NC], s1[NC];
+        Nb s0[NC], s1[NC], s2[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) { s0[c] = nb[c][0]; s1[c] = nb[c][1]; }
-        double fk[NC], fw[NC];
+        for (int c = 0; c < NC; ++c) { s0[c] = nb[c][0]; s1[c] = nb[c][1]; s2[c] = nb[c][2]; }
+        double fk[NC], fw[NC], fu[NC];
         P::f(s0, fk, a.pc);
         P::f(s1, fw, a.pc);
+        P::f(s2, fu, a.pc);  // f(u_n)
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-            val[c] = (fk[c] - fuc[c]) - dv(fw[c] - fuc[c], ctl.eps_d);  // integrators.py:106
+            val[c] = (fk[c] - fu[c]) - dv(fw[c] - fu[c], ctl.eps_d);  // integrators.py:106
     } else if constexpr (EV == EV_REMLIN) {
         Nb s0[NC], s1[NC];
 #pragma unroll
@@ -346,17 +356,18 @@ __device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
         for (int c = 0; c < NC; ++c) val[c] = (fk[c] - fuc[c]) - jd[c];
     } else {  // EV_REMBURG
         if constexpr (NC == 1 && NCH == 3) {
-            Nb s0[1] = {nb[0][0]};
-            double fk[1];
+            Nb s0[1] = {nb[0][0]}, s1[1] = {nb[0][1]};
+            double fk[1], fu[1];
             P::f(s0, fk, a.pc);
-            val[0] = (fk[0] - fuc[0]) - PBurgers::jac(nb[0][1], nb[0][2], a.pc);
+            P::f(s1, fu, a.pc);  // f(u_n) from the u channel
+            val[0] = (fk[0] - fu[0]) - PBurgers::jac(nb[0][1], nb[0][2], a.pc);
         }
     }
 }
 
 template <int EV>
 __host__ __device__ constexpr bool needs_fu() {
-    return EV == EV_FD || EV == EV_REMFD || EV == EV_REMLIN || EV == EV_REMBURG;
+    return EV == EV_REMLIN;
 }
 
 // Read the state scalars; false = the iteration has already terminated.

@@ -109,6 +109,7 @@ __device__ __forceinline__ void make_ch(const Ctl& ctl, const double (&r)[NR], d
     } else if constexpr (EV == EV_FD) {
         const double yv = ctl.has_div ? dv(r[1], ctl.ydiv) : r[1];
         ch[0] = r[0] + ctl.eps * yv;  // u + eps*v   (linalg.py:126)
+        ch[1] = r[0];                 // u: f(u_n) is re-evaluated, not streamed
     } else if constexpr (EV == EV_LIN) {
         ch[0] = ctl.has_div ? dv(r[0], ctl.ydiv) : r[0];
     } else if constexpr (EV == EV_BURGJ) {
@@ -117,6 +118,7 @@ __device__ __forceinline__ void make_ch(const Ctl& ctl, const double (&r)[NR], d
     } else if constexpr (EV == EV_REMFD) {
         ch[0] = r[0];
         ch[1] = r[1] + ctl.eps * (r[0] - r[1]);  // u + eps*(k - u)
+        ch[2] = r[1];
     } else if constexpr (EV == EV_REMLIN) {
         ch[0] = r[0];
         ch[1] = r[0] - r[1];

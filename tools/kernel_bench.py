@@ -64,7 +64,7 @@ def main():
     n = sys_._u.numel()
     fd = prof[0]["fd"]
     lin = args.problem in ("advdiff2d", "advdiff3d")
-    base = 4 if fd else (2 if lin else 3)
+    base = 3 if fd else (2 if lin else 3)  # FD: u, y read, y' written (f(u_n) recomputed)
     per = 8 * n * (base + 2 * args.k)
     out = {"problem": args.problem, "tma_mode": args.tma_mode,
            "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
@@ -93,7 +93,7 @@ def main():
         torch.cuda.synchronize()
         tk = e0.elapsed_time(e1) / 1e3
         # per Arnoldi step (FD, p_nz = 1): pass A 8N(5+1), B 8N*4, C 8N*2 (n+p ~ n)
-        perk = 8 * n * ((4 if fd else (2 if lin else 3)) + 1 + 1 + 1 + 4 + 2)
+        perk = 8 * n * ((3 if fd else (2 if lin else 3)) + 1 + 1 + 1 + 4 + 2)
         print(json.dumps({"kiops_steps": args.iters, "ms_per_arnoldi_step_incl_host":
                           tk / args.iters * 1e3, "bytes_per_step": perk,
                           "GBps_incl_host": perk * args.iters / tk / 1e9}))
