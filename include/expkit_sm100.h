@@ -108,6 +108,10 @@ typedef struct ek_leja_state {
                            p_i holds d_i[0] b, 0 while the first fused
                            iteration (m = 1) still has to write it       */
     double part[2];     /* local ||y||^2 and non-finite count                */
+    int32_t lazy0;      /* host: 1 = if everything freezes at m = 0, do not
+                           write p_i = d_i[0] b (the caller uses d_i[0]*b as
+                           an expression, ek_lincomb mode 3)                 */
+    int32_t pad_;
 } ek_leja_state;
 
 /* Scalar reduction slot (norms, dots, flags), device memory. */
@@ -349,15 +353,17 @@ int ek_vexpr(int64_t len, const int32_t* prog, int nprog,
              void* stream);
 /* Fused linear combinations (the stage algebra's fast path): output o is
  * fin_o(((t_0 + t_1) + t_2) + ...) with t = in[src] (mode 0), coef*in[src]
- * (mode 1) or in[src]/coef (mode 2); fin: 0 none, 1 multiply by fval,
- * 2 divide by fval. src / mode / coef are nout x 6 row-major. out[o] may be
+ * (mode 1), in[src]/coef (mode 2) or coef*(coef2*in[src]) (mode 3: a Leja
+ * result that froze at m = 0, d_0*b, consumed without being stored); fin:
+ * 0 none, 1 multiply by fval, 2 divide by fval. src / mode / coef / coef2
+ * are nout x 6 row-major (coef2 may be NULL without mode 3). out[o] may be
  * NULL (not stored). rmode 1 reduces output 0, rmode 2 the difference
  * out0 - out1 (err = ||u5 - u4||): st->val[0] = ||.||^2, val[1] = ||.||,
  * flag bit0 any nonzero, bit1 any non-finite. */
 int ek_lincomb(int64_t len, const double* const* in, int nin,
                double* const* out, int nout, const int32_t* nterm,
                const int32_t* src, const int32_t* mode, const double* coef,
-               const int32_t* fin, const double* fval, int rmode,
+               const double* coef2, const int32_t* fin, const double* fval, int rmode,
                ek_scalar_state* st, double* work, void* stream);
 /* ||x||^2 -> st->val[slot], ||x|| -> st->val[slot+1]; st->flag bit0 any
  * nonzero, bit1 any non-finite. */

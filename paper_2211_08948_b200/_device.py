@@ -217,8 +217,8 @@ class Expr:
 
 
 def V(t):
-    """Leaf for a device vector."""
-    return Expr("vec", t)
+    """Leaf for a device vector (an Expr passes through: lazy engine results)."""
+    return t if isinstance(t, Expr) else Expr("vec", t)
 
 
 _OPC = {"add": N.VX_ADD, "sub": N.VX_SUB, "mul": N.VX_MUL, "div": N.VX_DIV}
@@ -256,19 +256,36 @@ class _Prog:
             self.emit(_OPC[e.op])
 
 
-LT_X, LT_MUL, LT_DIV = 0, 1, 2
+LT_X, LT_MUL, LT_DIV, LT_MUL2 = 0, 1, 2, 3
 LC_IN, LC_OUT, LC_TERMS = 8, 3, 6
 
 
+def _scaled_vec(e):
+    """(tensor, c) for c*x / x*c, else None."""
+    if e.op == "mul":
+        if e.a.op == "const" and e.b.op == "vec":
+            return e.b.a, e.a.a
+        if e.b.op == "const" and e.a.op == "vec":
+            return e.a.a, e.b.a
+    return None
+
+
 def _term(e):
-    """(tensor, mode, coef) for x, c*x, x*c, x/c, -x, -(c*x); else None."""
+    """(tensor, mode, coef[, coef2]) for x, c*x, x*c, x/c, c1*(c2*x), -x,
+    -(c*x); else None."""
     if e.op == "vec":
         return (e.a, LT_X, 1.0)
     if e.op == "mul":
-        if e.a.op == "const" and e.b.op == "vec":
-            return (e.b.a, LT_MUL, e.a.a)
-        if e.b.op == "const" and e.a.op == "vec":
-            return (e.a.a, LT_MUL, e.b.a)
+        sv = _scaled_vec(e)
+        if sv is not None:
+            return (sv[0], LT_MUL, sv[1])
+        # c1 * (c2 * x): a lazy m = 0 Leja result d0*b scaled by a stage weight
+        if e.a.op == "const" and _scaled_vec(e.b) is not None:
+            x, c2 = _scaled_vec(e.b)
+            return (x, LT_MUL2, e.a.a, c2)
+        if e.b.op == "const" and _scaled_vec(e.a) is not None:
+            x, c2 = _scaled_vec(e.a)
+            return (x, LT_MUL2, e.b.a, c2)
     if e.op == "div" and e.a.op == "vec" and e.b.op == "const":
         return (e.a.a, LT_DIV, e.b.a)
     if e.op == "neg":
@@ -279,12 +296,13 @@ def _term(e):
 
 
 def _negate(t):
-    # a - x == a + (-1)*x, a - c*x == a + (-c)*x, a - x/c == a + x/(-c):
-    # each is bit-identical in IEEE arithmetic (negation is exact)
-    v, m, c = t
+    # a - x == a + (-1)*x, a - c*x == a + (-c)*x, a - x/c == a + x/(-c),
+    # a - c1*(c2*x) == a + (-c1)*(c2*x): each is bit-identical in IEEE
+    # arithmetic (negation is exact)
+    v, m, c = t[:3]
     if m == LT_X:
         return (v, LT_MUL, -1.0)
-    return (v, m, -c)
+    return (v, m, -c) + tuple(t[3:])
 
 
 def _chain(e):
@@ -341,19 +359,22 @@ def _lincomb(outputs, length, rmode):
     src = (C.c_int32 * (nout * LC_TERMS))()
     mode = (C.c_int32 * (nout * LC_TERMS))()
     coef = (C.c_double * (nout * LC_TERMS))()
+    coef2 = (C.c_double * (nout * LC_TERMS))()
     fin = (C.c_int32 * nout)()
     fval = (C.c_double * nout)()
     for o, (terms, fm, fv) in enumerate(folds):
         nterm[o] = len(terms)
-        for t, (v, m, c) in enumerate(terms):
+        for t, term in enumerate(terms):
+            v, m, c = term[:3]
             src[o * LC_TERMS + t] = idx(v)
             mode[o * LC_TERMS + t] = m
             coef[o * LC_TERMS + t] = float(c)
+            coef2[o * LC_TERMS + t] = float(term[3]) if len(term) > 3 else 0.0
         fin[o] = fm
         fval[o] = float(fv)
     if len(ins) > LC_IN:
         return False
-    return ins, nterm, src, mode, coef, fin, fval
+    return ins, nterm, src, mode, coef, coef2, fin, fval
 
 
 def evaluate(outputs, length, norm=False, check=False, norm_diff=False):
@@ -367,12 +388,12 @@ def evaluate(outputs, length, norm=False, check=False, norm_diff=False):
     rmode = 2 if norm_diff else (1 if (norm or check) else 0)
     low = _lincomb(outputs, length, rmode)
     if low:
-        ins, nterm, src, mode, coef, fin, fval = low
+        ins, nterm, src, mode, coef, coef2, fin, fval = low
         outs = [o for _, o in outputs]
         st = scalar_state() if rmode else None
         N.check(N.lib().ek_lincomb(
             int(length), N.ptrs(ins), len(ins), N.ptrs(outs), len(outs), nterm, src, mode,
-            coef, fin, fval, rmode, st.ptr if st else None, work_ptr() if st else None,
+            coef, coef2, fin, fval, rmode, st.ptr if st else None, work_ptr() if st else None,
             stream()), "ek_lincomb")
         if st is None:
             return None

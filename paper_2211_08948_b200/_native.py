@@ -39,7 +39,8 @@ class LejaState(C.Structure):
                 ("status", C.c_int32), ("k", C.c_int32), ("active", C.c_uint32),
                 ("fd_evals", C.c_int32), ("ticket", C.c_uint32),
                 ("iters", C.c_int32), ("freeze", C.c_int32 * 8), ("defer", C.c_int32),
-                ("p_init", C.c_int32), ("part", C.c_double * 2)]
+                ("p_init", C.c_int32), ("part", C.c_double * 2), ("lazy0", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class Peer(C.Structure):
@@ -124,8 +125,8 @@ _SIGS = {
     "ek_l1": (_I, [_L, _P, _P, _I, _P, _P]),
     "ek_selftest_div": (_I, [_L, _P, _P, _P, _P, _P]),
     "ek_lincomb": (_I, [_L, _PP, _I, _PP, _I, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
-                        C.POINTER(C.c_int32), C.POINTER(_D), C.POINTER(C.c_int32),
-                        C.POINTER(_D), _I, _P, _P, _P]),
+                        C.POINTER(C.c_int32), C.POINTER(_D), C.POINTER(_D),
+                        C.POINTER(C.c_int32), C.POINTER(_D), _I, _P, _P, _P]),
     "ek_dense_gemv": (_I, [_L, _P, _P, _P, _P]),
     "ek_ctx_create": (_P, [_I, _P]),
     "ek_ctx_destroy": (None, [_P]),

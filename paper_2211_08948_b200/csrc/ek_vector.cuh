@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
 // Folded begin: if every accumulator froze at m = 0 no iteration will write
 // the accumulators, so write p_i = d_i[0] b here (a no-op otherwise).
 __global__ void __launch_bounds__(TPB) k_leja_fold_done(const LejaVArgs a) {
-    if (!a.st->done || a.st->p_init != 0) return;
+    if (!a.st->done || a.st->p_init != 0 || a.st->lazy0) return;
     double d[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32] : 0.0;
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
 // a + (-c)*b, which is bit-identical). Output 0 may be "virtual" (not
 // stored) and is the one reduced: ||out0||^2 and nonzero / non-finite flags.
 constexpr int LC_IN = 8, LC_OUT = 3, LC_TERMS = 6;
-enum { LT_X = 0, LT_MUL = 1, LT_DIV = 2 };
+enum { LT_X = 0, LT_MUL = 1, LT_DIV = 2, LT_MUL2 = 3 };
 struct LincombArgs {
     int64_t len;
     const double* in[LC_IN];
@@ -588,7 +588,7 @@ struct LincombArgs {
     int nterm[LC_OUT];
     int src[LC_OUT][LC_TERMS];
     int mode[LC_OUT][LC_TERMS];
-    Dv coef[LC_OUT][LC_TERMS];   // c (LT_MUL: c.d is the factor) or divisor
+    Dv coef[LC_OUT][LC_TERMS];   // c (LT_MUL: c.d is the factor; LT_MUL2: c.d * (c.r * x)) or divisor
     int fin[LC_OUT];             // 0 none, 1 multiply, 2 divide
     Dv fval[LC_OUT];
     int reduce;
@@ -600,6 +600,7 @@ __device__ __forceinline__ double lc_term(const LincombArgs& a, int o, int t, do
     const int m = a.mode[o][t];
     if (m == LT_MUL) return a.coef[o][t].d * x;
     if (m == LT_DIV) return dv(x, a.coef[o][t]);
+    if (m == LT_MUL2) return a.coef[o][t].d * (a.coef[o][t].r * x);
     return x;
 }
 

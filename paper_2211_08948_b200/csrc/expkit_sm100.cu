@@ -689,8 +689,8 @@ int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot, double* w
 
 int ek_lincomb(int64_t len, const double* const* in, int nin, double* const* out, int nout,
                const int32_t* nterm, const int32_t* src, const int32_t* mode, const double* coef,
-               const int32_t* fin, const double* fval, int rmode, ek_scalar_state* st,
-               double* work, void* stream) {
+               const double* coef2, const int32_t* fin, const double* fval, int rmode,
+               ek_scalar_state* st, double* work, void* stream) {
     if (nin < 1 || nin > LC_IN || nout < 1 || nout > LC_OUT) {
         set_error("ek_lincomb: nin=%d nout=%d out of range", nin, nout);
         return EK_ERR_INVALID;
@@ -715,7 +715,13 @@ int ek_lincomb(int64_t len, const double* const* in, int nin, double* const* out
             }
             a.src[o][t] = src[k];
             a.mode[o][t] = mode[k];
-            a.coef[o][t] = mode[k] == LT_DIV ? mkdv(coef[k]) : Dv{coef[k], 0.0};
+            if (mode[k] == LT_MUL2 && !coef2) {
+                set_error("ek_lincomb: mode 3 needs coef2");
+                return EK_ERR_INVALID;
+            }
+            a.coef[o][t] = mode[k] == LT_DIV    ? mkdv(coef[k])
+                         : mode[k] == LT_MUL2 ? Dv{coef[k], coef2[k]}
+                                              : Dv{coef[k], 0.0};
         }
         a.fin[o] = fin[o];
         a.fval[o] = fin[o] == 2 ? mkdv(fval[o]) : Dv{fval[o], 0.0};

@@ -23,6 +23,7 @@ from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
+import torch
 
 from . import _device as D
 from . import _native as N
@@ -190,13 +191,18 @@ def _slab_decide(st, Jn, table, base, m, k, begin):
 
 
 def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
-                              xi=None, max_points=DEFAULT_NUM_POINTS):
+                              xi=None, max_points=DEFAULT_NUM_POINTS, _lazy_m0=False):
     """phi_l(c_i h J) b for several scale factors c_i sharing one Newton
     basis recurrence (leja.py:133-189). Accumulator i freezes once
     |d_i[m]| ||y_m|| < tol; the loop runs until all are frozen.
 
     Returns LejaResult(vectors, iters, freeze_iters); raises NonConvergence
-    after `max_points` terms or on a non-finite ||y||."""
+    after `max_points` terms or on a non-finite ||y||.
+
+    _lazy_m0 (integrator engines only, device b): if every accumulator
+    freezes at m = 0 the results d_i[0]*b are returned as expressions
+    (`_device.Expr`) that the stage algebra evaluates in registers with the
+    same rounding, instead of being written to HBM."""
     if tol <= 0:
         raise ValueError("tolerance must be positive")
     if len(coeffs) < 1:
@@ -231,8 +237,9 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     # fused single-GPU path: the begin pass only takes ||b|| and the m = 0
     # decisions; the first iteration writes p_i = d_i[0] b + d_i[1] y_1
     fold = Jn is not None and not slab and max_points > 1
+    lazy = bool(_lazy_m0 and fold and isinstance(b, torch.Tensor))
     st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k, defer=1 if slab else 0,
-                    p_init=-1 if fold else 0)
+                    p_init=-1 if fold else 0, lazy0=1 if lazy else 0)
     ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(Jn.grid)) if Jn else None)
     pp = N.ptrs(ps)
     N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()), pp, k,
@@ -269,7 +276,6 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             # the rest of the chunk; kernels after termination early-exit
             hi = min(m_avail, m + 8) if m == 1 else m_avail
             if prof is not None:
-                import torch
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
             if slab and Jn.comm.peer:
@@ -330,6 +336,10 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
         if hst.status == N.ST_PEER_TIMEOUT:
             raise RuntimeError("peer mode: a rank's pass flag did not arrive (dead peer?)")
         if hst.done:
+            if lazy and int(hst.iters) == 0:
+                # everything froze at m = 0: ps[i] = dds[i][0] * y (leja.py:161)
+                return LejaResult(vectors=[float(dds[i][0]) * D.V(bd) for i in range(k)],
+                                  iters=0, freeze_iters=[0] * k)
             return LejaResult(vectors=[D.like_input(p, b) for p in ps],
                               iters=int(hst.iters),
                               freeze_iters=[int(hst.freeze[i]) for i in range(k)])
