@@ -248,10 +248,16 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
     if constexpr (P::DIM == 2) {
         TmaMaps maps;
         // auto (3): the row march where it measured faster on the B200 (Leja
-        // with k >= 3 accumulators: 0.436 vs 0.498 ms at k = 3, config 4),
-        // 32 x 8 chunks otherwise (k = 2: 0.340 vs 0.392 ms, k = 1: 0.252
-        // vs 0.347 ms)
-        const bool march = g_tma_mode == 2 || (g_tma_mode == 3 && EP == EP_LEJA && K >= 3);
+        // with k >= 3 ACTIVE accumulators: 0.436 vs 0.498 ms at k = 3, config
+        // 4), 32 x 8 chunks otherwise (k = 2: 0.340 vs 0.392 ms, k = 1: 0.252
+        // vs 0.347 ms). The active count changes on the device as
+        // accumulators freeze, so a K >= 3 Leja iteration off slab mode is
+        // launched as a pair — march (runs iff >= 3 active) then chunks (runs
+        // iff <= 2 active) — and exactly one of them does the pass (the
+        // other exits at its first read of the state block).
+        const bool pair = g_tma_mode == 3 && EP == EP_LEJA && K >= 3 && !a.g.slab &&
+                          march_ok(a);
+        const bool march = g_tma_mode == 2 || pair;
         if (march && march_ok(a)) {
             constexpr int S = tma_stages2<EV, EP, P::NC, K>();
             constexpr int SMEM = S * stage2_doubles<EV, EP, P::NC, K>() * 8;
@@ -269,9 +275,11 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
             int64_t ng = cap >= ns ? cap / ns : 1;
             if (ng > a.g.rows / 8) ng = a.g.rows / 8 > 0 ? a.g.rows / 8 : 1;
             const unsigned grid = (unsigned)(cap >= ns ? ns * ng : cap);
-            kern<<<grid, T2, SMEM, s>>>(a);
+            KArgs am = a;
+            if (pair) { am.act_lo = 3; am.act_hi = 8; }
+            kern<<<grid, T2, SMEM, s>>>(am);
             EK_LAUNCH_CHECK("bulk-copy march stencil launch");
-            return EK_OK;
+            if (!pair) return EK_OK;
         }
         if (g_tma_mode != 0 && tma_ok(a) && build_maps<EV, EP, P::NC, K>(a, maps)) {
             constexpr int S = tma_stages<EV, EP, P::NC, K>();
@@ -287,7 +295,9 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
             const int64_t chunks = ((a.g.n + 31) / 32) * ((a.g.rows + 7) / 8);
             const int64_t cap = (int64_t)sm_count() * tocc;
             const unsigned grid = (unsigned)(chunks < cap ? chunks : cap);
-            kern<<<grid, TPB, SMEM, s>>>(a, maps);
+            KArgs ac = a;
+            if (pair) { ac.act_lo = 0; ac.act_hi = 2; }
+            kern<<<grid, TPB, SMEM, s>>>(ac, maps);
             EK_LAUNCH_CHECK("tma stencil launch");
             return EK_OK;
         }

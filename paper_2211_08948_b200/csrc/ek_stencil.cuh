@@ -220,6 +220,9 @@ struct KArgs {
     // number; null off that mode
     const ek_peer* peer;
     long epoch;
+    // Leja pair launches (ek_launch.cuh): run only if act_lo <= #active <=
+    // act_hi and iteration m-1 is the last finalised one; 0 / 0 = always
+    int act_lo, act_hi;
 };
 
 // ----------------------------------------------------------------- geometry
@@ -384,6 +387,10 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     if constexpr (EP == EP_LEJA) {
         const ek_leja_state* st = (const ek_leja_state*)a.st;
         if (st->done) return false;
+        if (a.act_hi > 0) {
+            const int na = __popc(st->active);
+            if (na < a.act_lo || na > a.act_hi || st->m != a.m - 1) return false;
+        }
         ctl.eps = st->eps;
         ctl.active = st->active;
         ctl.y_zero = (EV == EV_FD) && (st->ny == 0.0);
