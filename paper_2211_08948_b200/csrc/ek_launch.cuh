@@ -251,12 +251,13 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
         // with k >= 3 ACTIVE accumulators: 0.436 vs 0.498 ms at k = 3, config
         // 4), 32 x 8 chunks otherwise (k = 2: 0.340 vs 0.392 ms, k = 1: 0.252
         // vs 0.347 ms). The active count changes on the device as
-        // accumulators freeze, so a K >= 3 Leja iteration off slab mode is
-        // launched as a pair — march (runs iff >= 3 active) then chunks (runs
-        // iff <= 2 active) — and exactly one of them does the pass (the
-        // other exits at its first read of the state block).
-        const bool pair = g_tma_mode == 3 && EP == EP_LEJA && K >= 3 && !a.g.slab &&
-                          march_ok(a);
+        // accumulators freeze, so a K >= 3 Leja iteration is launched as a
+        // pair — march (runs iff >= 3 active) then chunks (runs iff <= 2
+        // active) — and exactly one of them does the pass (the other exits at
+        // its first read of the state block: if the march ran, it advanced
+        // st->m; in slab mode the decision waits for the decide kernel, so
+        // the count the chunk kernel reads is still the one the march saw).
+        const bool pair = g_tma_mode == 3 && EP == EP_LEJA && K >= 3 && march_ok(a);
         const bool march = g_tma_mode == 2 || pair;
         if (march && march_ok(a)) {
             constexpr int S = tma_stages2<EV, EP, P::NC, K>();
