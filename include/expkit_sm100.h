@@ -199,6 +199,17 @@ int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu,
 int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu,
                  const double* k, double eps, double* out, ek_scalar_state* st,
                  double* work, const double* const* halo, void* stream);
+/* The remainder pass fused with the stage algebra that consumes R: besides
+ * (or instead of, out = NULL) R it stores nx <= 3 vectors
+ *   xo[q] = ((xa[q] * xin) + (xr[q] * R)) * xf[q]     (xin != NULL)
+ *   xo[q] = (xr[q] * R) * xf[q]                       (xin == NULL)
+ * in NumPy's rounding order, e.g. R(a)*dt or ((-2 R(a)) + R(b))*dt of
+ * EPIRK5P1 (integrators.py:318-341), without writing R and re-reading it. */
+int ek_remainder_combo(const ek_grid* g, int jac, const double* u, const double* fu,
+                       const double* k, double eps, double* out, int nx, double* const* xo,
+                       const double* xin, const double* xa, const double* xr,
+                       const double* xf, ek_scalar_state* st, double* work,
+                       const double* const* halo, void* stream);
 
 /* ------------------------------------------------------- Leja (leja.py) */
 /* Coefficient table coef_dev: (k+1) rows x 32 columns, row 0 the shifts

@@ -233,6 +233,9 @@ inline bool build_maps(const KArgs& a, TmaMaps& m) {
     if constexpr (EP == EP_LEJA)
         for (int q = 0; q < K && q < a.nk; ++q)
             if (!mk(&m.m[t++], a.p[q], cw, ch)) return false;
+    if constexpr (EP == EP_REM)
+        for (int q = 0; q < K; ++q)
+            if (!mk(&m.m[t++], a.xin, cw, ch)) return false;
     if constexpr (EP == EP_ARN)
         for (int q = 0; q < K && q < a.nwin + a.naug; ++q) {
             const double* f = arn_slot(a, q);
@@ -355,6 +358,8 @@ inline int launch_p(const KArgs& a, cudaStream_t s) {
             default: return launch_k<P, EV, EP, 8>(a, s);
         }
     } else {
+        if constexpr (EP == EP_REM)
+            if (a.xin) return launch_k<P, EV, EP, 1>(a, s);  // centre slot: xin
         return launch_k<P, EV, EP, 0>(a, s);
     }
 }

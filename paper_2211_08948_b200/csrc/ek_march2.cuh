@@ -82,6 +82,7 @@ __device__ __forceinline__ const double* ctr_field(const KArgs& a, int g) {
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     if (g < FU) return a.fu;
     if constexpr (EP == EP_ARN) return arn_slot(a, g - FU);
+    if constexpr (EP == EP_REM) return a.xin;
     return a.p[g - FU];
 }
 
@@ -183,6 +184,7 @@ __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, con
                 z.p[q][c] = (EP == EP_ARN && q == a.nwin - 1)
                                 ? yc[c] : ctr[((FU + q) * NC + c) * CTR2 + t];
         }
+        if constexpr (EP == EP_REM && K > 0) z.p[0][c] = ctr[(FU * NC + c) * CTR2 + t];
     }
     double val[NC];
     evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);

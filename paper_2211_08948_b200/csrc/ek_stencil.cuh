@@ -223,6 +223,12 @@ struct KArgs {
     // Leja pair launches (ek_launch.cuh): run only if act_lo <= #active <=
     // act_hi and iteration m-1 is the last finalised one; 0 / 0 = always
     int act_lo, act_hi;
+    // EP_REM secondary outputs (ek_remainder_combo): xo[q] = ((xa[q] * xin)
+    // + (xr[q] * R)) * xf[q], or (xr[q] * R) * xf[q] without xin
+    double* xo[3];
+    const double* xin;
+    double xa[3], xr[3], xf[3];
+    int nxo;
 };
 
 // ----------------------------------------------------------------- geometry
@@ -428,6 +434,7 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
                            ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
         }
     }
+    if constexpr (EP == EP_REM) ctl.active = a.xin ? 1u : 0u;  // centre slot 0 = xin
     ctl.h_first = ctl.h_second = ctl.h_penult = ctl.h_last = nullptr;
     ctl.rowlen = 0;
     if constexpr (EP == EP_LEJA) {
@@ -501,6 +508,8 @@ __device__ __forceinline__ void load_centre(const KArgs& a, const Ctl& ctl, long
 #pragma unroll
             for (int q = 0; q < K; ++q)
                 z.p[q][c] = q < a.nwin + a.naug ? __ldg(arn_slot(a, q) + e) : 0.0;
+        } else if constexpr (EP == EP_REM && K > 0) {
+            z.p[0][c] = __ldg(a.xin + e);  // input of the secondary outputs
         }
     }
 }
@@ -561,7 +570,18 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
                 if (q < a.nwin) acc[q] += z.p[q][c] * w;
             if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
         } else {  // EP_REM
-            st_stream(a.out + e, v, ctl.wpol);
+            if (a.out) st_stream(a.out + e, v, ctl.wpol);
+            if (a.nxo) {  // the stage algebra that consumes R, in registers
+                const double xin = K > 0 ? z.p[0][c] : 0.0;  // staged with the pass
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    if (q < a.nxo) {
+                        const double rv = a.xr[q] * v;
+                        const double t = K > 0 ? (a.xa[q] * xin) + rv : rv;
+                        st_stream(a.xo[q] + e, t * a.xf[q], ctl.wpol);
+                    }
+                }
+            }
             acc[0] += isfinite(v) ? 0.0 : 1.0;
         }
     }

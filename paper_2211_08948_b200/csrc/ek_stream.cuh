@@ -133,7 +133,7 @@ __device__ __forceinline__ void make_ch(const Ctl& ctl, const double (&r)[NR], d
 // Arnoldi window rows followed by the augmentation vectors
 template <int EV, int EP, int K>
 __host__ __device__ constexpr int nctr_maps() {
-    return (needs_fu<EV>() ? 1 : 0) + ((EP == EP_LEJA || EP == EP_ARN) ? K : 0);
+    return (needs_fu<EV>() ? 1 : 0) + ((EP == EP_LEJA || EP == EP_ARN || EP == EP_REM) ? K : 0);
 }
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage_doubles() {
@@ -240,6 +240,7 @@ __device__ __forceinline__ void tma_point(const KArgs& a, const Ctl& ctl, const 
                 z.p[q][c] = (EP == EP_ARN && q == a.nwin - 1)
                                 ? yc[c] : ctr[((FU + q) * NC + c) * CTR_SLOT + co];
         }
+        if constexpr (EP == EP_REM && K > 0) z.p[0][c] = ctr[(FU * NC + c) * CTR_SLOT + co];
     }
     double val[NC];
     evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);

@@ -177,6 +177,7 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
                 z.p[q][c] = (EP == EP_ARN && q == a.nwin - 1)
                                 ? yc[c] : ctr[((FU + q) * NC + c) * CTR3 + co];
         }
+        if constexpr (EP == EP_REM && K > 0) z.p[0][c] = ctr[(FU * NC + c) * CTR3 + co];
     }
     double val[NC];
     evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);

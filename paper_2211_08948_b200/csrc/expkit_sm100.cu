@@ -307,6 +307,42 @@ int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu, c
     return launch_stencil<EP_REM>(ev, a, (cudaStream_t)stream);
 }
 
+int ek_remainder_combo(const ek_grid* g, int jac, const double* u, const double* fu,
+                       const double* k, double eps, double* out, int nx, double* const* xo,
+                       const double* xin, const double* xa, const double* xr, const double* xf,
+                       ek_scalar_state* st, double* work, const double* const* halo,
+                       void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (nx < 0 || nx > 3 || (nx > 0 && (!xo || !xr || !xf || (xin && !xa))) || (!out && nx == 0)) {
+        set_error("ek_remainder_combo: bad outputs (nx=%d)", nx);
+        return EK_ERR_INVALID;
+    }
+    if (g->problem == EK_P_SEMILINEAR) {
+        set_error("semilinear remainder runs through the generic path");
+        return EK_ERR_UNSUPPORTED;
+    }
+    int ev;
+    if (jac == EK_JAC_FD) ev = EV_REMFD;
+    else if (analytic_ev(g) == EV_LIN) ev = EV_REMLIN;
+    else if (analytic_ev(g) == EV_BURGJ) ev = EV_REMBURG;
+    else {
+        set_error("problem %d has no analytic Jacobian stencil", g->problem);
+        return EK_ERR_UNSUPPORTED;
+    }
+    KArgs a;
+    base_args(a, g, halo);
+    a.u = u; a.fu = fu; a.k = k; a.eps = eps; a.out = out; a.st = st; a.work = work;
+    a.nxo = nx;
+    a.xin = xin;
+    for (int q = 0; q < nx; ++q) {
+        a.xo[q] = xo[q];
+        a.xa[q] = xin ? xa[q] : 0.0;
+        a.xr[q] = xr[q];
+        a.xf[q] = xf[q];
+    }
+    return launch_stencil<EP_REM>(ev, a, (cudaStream_t)stream);
+}
+
 // ------------------------------------------------------------------- Leja
 // m = 0 over a flat vector of length len (the state block must hold tol,
 // nu and k; see ek_leja_state).

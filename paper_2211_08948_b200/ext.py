@@ -177,13 +177,15 @@ def step_exprb32(sys, dt, scheme, tol, ctx):
     n = u.numel()
     fdt = D.ev(X(sys._f) * dt)
     if scheme == "leja":
-        a, Ra = eng.stage_remainder(X(u) + X(eng.leja_single("internal", fdt, 1, dt)),
-                                    keep=True)
-        t3 = eng.leja_single("stage3", D.ev((2.0 * X(Ra)) * dt), 3, dt)
+        a, (_, (r2,)) = eng.stage_remainder(
+            X(u) + X(eng.leja_single("internal", fdt, 1, dt)), keep=True,
+            combos=[(None, 0.0, 2.0, dt)], store=False)  # (2 R(a)) dt
+        t3 = eng.leja_single("stage3", r2, 3, dt)
     else:
-        a, Ra = eng.stage_remainder(X(u) + X(eng.kiops_combo("internal", [None, fdt], dt)),
-                                    keep=True)
-        t3 = eng.kiops_combo("stage3", [None, None, None, D.ev((2.0 * X(Ra)) * dt)], dt)
+        a, (_, (r2,)) = eng.stage_remainder(
+            X(u) + X(eng.kiops_combo("internal", [None, fdt], dt)), keep=True,
+            combos=[(None, 0.0, 2.0, dt)], store=False)
+        t3 = eng.kiops_combo("stage3", [None, None, None, r2], dt)
     u3 = D.ev(X(a) + X(t3))
     err = D.evaluate([(X(u3) - X(a), None)], n, norm=True)[0]
     return StepResult(u3, err, stats, sys._as_numpy)
