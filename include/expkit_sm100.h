@@ -183,6 +183,11 @@ int ek_sync(void* stream);
  * {u_halo, y_halo, k_halo} for a slab. */
 int ek_rhs(const ek_grid* g, const double* u, double* out,
            const double* const* halo, void* stream);
+/* f(u) as ek_rhs, plus ||u||^2 -> st->val[0], ||u|| -> st->val[1], flag
+ * bit0 any nonzero, bit1 any non-finite (the ||u|| of linalg.py:123 that
+ * an FD linearisation needs, from the same pass). 2-D / 3-D grids. */
+int ek_rhs_norm(const ek_grid* g, const double* u, double* out, ek_scalar_state* st,
+                double* work, const double* const* halo, void* stream);
 
 /* out = J(u) v.  jac = EK_JAC_FD: (f(u+eps v) - fu)/eps with the caller's
  * eps = (sqrt(eps_mach)*(1+||u||))/||v|| (linalg.py:111-129); when `st` is

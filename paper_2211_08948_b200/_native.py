@@ -92,6 +92,7 @@ _SIGS = {
     "ek_copy": (_I, [_P, _P, _L, _I, _P]),
     "ek_sync": (_I, [_P]),
     "ek_rhs": (_I, [C.POINTER(Grid), _P, _P, _PP, _P]),
+    "ek_rhs_norm": (_I, [C.POINTER(Grid), _P, _P, _P, _P, _PP, _P]),
     "ek_jv": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _P, _P, _PP, _P]),
     "ek_remainder": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _P, _P, _PP, _P]),
     "ek_remainder_combo": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _I, _PP, _P,

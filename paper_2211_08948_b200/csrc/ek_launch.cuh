@@ -370,7 +370,7 @@ template <class P, int EP>
 inline int launch_ev(int ev, const KArgs& a, cudaStream_t s) {
     switch (ev) {
         case EV_RHS:
-            if constexpr (EP == EP_STORE) return launch_p<P, EV_RHS, EP>(a, s);
+            if constexpr (EP == EP_STORE || EP == EP_RHSN) return launch_p<P, EV_RHS, EP>(a, s);
             break;
         case EV_FD:
             if constexpr (EP != EP_REM) return launch_p<P, EV_FD, EP>(a, s);
@@ -419,6 +419,7 @@ inline int launch_problem(int ep, int ev, const KArgs& a, cudaStream_t s) {
         case EP_POWER: return launch_ev<P, EP_POWER>(ev, a, s);
         case EP_ARN: return launch_ev<P, EP_ARN>(ev, a, s);
         case EP_REM: return launch_ev<P, EP_REM>(ev, a, s);
+        case EP_RHSN: return launch_ev<P, EP_RHSN>(ev, a, s);
     }
     set_error("unsupported epilogue %d", ep);
     return EK_ERR_UNSUPPORTED;

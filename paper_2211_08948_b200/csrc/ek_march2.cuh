@@ -177,6 +177,7 @@ __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, con
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         z.fu[c] = FU ? ctr[c * CTR2 + t] : 0.0;
+        if constexpr (EP == EP_RHSN) z.y[c] = yc[c];  // u at the centre
         if constexpr (EP == EP_LEJA || EP == EP_ARN) {
             z.y[c] = yc[c];
 #pragma unroll

@@ -17,6 +17,9 @@
 //     EP_POWER   w = value ; ||w||^2 ; convergence test (spectrum.py:56-63)
 //     EP_ARN     w = dt*value + tail@uflip ; window dots (kiops.py:182-187)
 //     EP_REM     out = value ; non-finite flag (integrators.py:107-108)
+//     EP_RHSN    out = f(u) ; ||u||^2 and nonzero / non-finite flags of u
+//                (the RHS pass of a linearisation also yields linalg.py:123's
+//                ||u||, one vector pass less)
 //
 // Geometry: a warp owns 32 consecutive columns of the contiguous axis (one
 // lane per column, coalesced 256-B segments) and marches RPT consecutive
@@ -45,7 +48,7 @@
 namespace ek {
 
 enum { EV_RHS = 0, EV_FD, EV_LIN, EV_BURGJ, EV_REMFD, EV_REMLIN, EV_REMBURG };
-enum { EP_STORE = 0, EP_LEJA, EP_POWER, EP_ARN, EP_REM };
+enum { EP_STORE = 0, EP_LEJA, EP_POWER, EP_ARN, EP_REM, EP_RHSN };
 
 // Channels per point. EV_FD / EV_REMFD carry u itself as the last channel:
 // f(u_n) is re-evaluated from the u neighbourhood the pass reads anyway
@@ -56,7 +59,8 @@ __host__ __device__ constexpr int ev_nch(int ev) {
          : ev == EV_REMBURG ? 3 : 1;
 }
 __host__ __device__ constexpr int ep_nq(int ep) {
-    return ep == EP_LEJA ? 2 : ep == EP_POWER ? 2 : ep == EP_ARN ? 5 : ep == EP_REM ? 1 : 0;
+    return ep == EP_LEJA ? 2 : ep == EP_POWER ? 2 : ep == EP_ARN ? 5 : ep == EP_REM ? 1
+         : ep == EP_RHSN ? 3 : 0;
 }
 
 struct Nb {
@@ -499,6 +503,7 @@ __device__ __forceinline__ void load_centre(const KArgs& a, const Ctl& ctl, long
         const long e = c * a.npts + off;
         if constexpr (needs_fu<EV>()) z.fu[c] = __ldg(a.fu + e);
         else z.fu[c] = 0.0;
+        if constexpr (EP == EP_RHSN) z.y[c] = __ldg(a.u + e);
         if constexpr (EP == EP_LEJA) {
             z.y[c] = __ldg(a.y + e);
 #pragma unroll
@@ -532,6 +537,12 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
         const double v = val[c];
         if constexpr (EP == EP_STORE) {
             st_stream(a.out + e, v, ctl.wpol);
+        } else if constexpr (EP == EP_RHSN) {
+            st_stream(a.out + e, v, ctl.wpol);
+            const double uc = z.y[c];
+            acc[0] += uc * uc;
+            acc[1] += uc != 0.0 ? 1.0 : 0.0;
+            acc[2] += isfinite(uc) ? 0.0 : 1.0;
         } else if constexpr (EP == EP_LEJA) {
             // y = J.apply(y)/gamma - (c/gamma + xi[m-1]) * y      leja.py:172
             const double yn = dv(v, a.gamma) - (ctl.shift * z.y[c]);
@@ -797,6 +808,13 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
 
 template <int EV, int EP>
 __device__ void finalize(const KArgs& a, const double* tot) {
+    if constexpr (EP == EP_RHSN) {
+        ek_scalar_state* st = (ek_scalar_state*)a.st;
+        st->val[0] = tot[0];
+        st->val[1] = sqrt(tot[0]);
+        st->flag |= (tot[1] > 0.0 ? 1 : 0) | (tot[2] > 0.0 ? 2 : 0);
+        return;
+    }
     if constexpr (EP == EP_LEJA) {
         ek_leja_state* st = (ek_leja_state*)a.st;
         st->p_init = 1;

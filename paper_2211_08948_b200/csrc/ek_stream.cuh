@@ -233,6 +233,7 @@ __device__ __forceinline__ void tma_point(const KArgs& a, const Ctl& ctl, const 
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         z.fu[c] = FU ? ctr[c * CTR_SLOT + co] : 0.0;
+        if constexpr (EP == EP_RHSN) z.y[c] = yc[c];  // u at the centre
         if constexpr (EP == EP_LEJA || EP == EP_ARN) {
             z.y[c] = yc[c];
 #pragma unroll

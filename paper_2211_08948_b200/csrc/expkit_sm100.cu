@@ -257,6 +257,22 @@ int ek_rhs(const ek_grid* g, const double* u, double* out, const double* const* 
     return launch_stencil<EP_STORE>(EV_RHS, a, s);
 }
 
+int ek_rhs_norm(const ek_grid* g, const double* u, double* out, ek_scalar_state* st,
+                double* work, const double* const* halo, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (g->dim < 2 || !st || !work) {
+        set_error("ek_rhs_norm: 2-D / 3-D stencil grids with a state block and workspace");
+        return EK_ERR_INVALID;
+    }
+    KArgs a;
+    base_args(a, g, halo);
+    a.u = u;
+    a.out = out;
+    a.st = st;
+    a.work = work;
+    return launch_stencil<EP_RHSN>(EV_RHS, a, (cudaStream_t)stream);
+}
+
 int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu, const double* v,
           double eps, double* out, ek_scalar_state* st, double* work,
           const double* const* halo, void* stream) {

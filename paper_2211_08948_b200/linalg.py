@@ -197,7 +197,12 @@ class NativeJacobian(MatrixFreeOperator):
     def nu(self):
         """||u|| (linalg.py:123), computed once per linearisation."""
         if self._nu is None:
-            self._nu = D.norm2(self.u)[0] if self.jac == N.JAC_FD else 0.0
+            if self.jac != N.JAC_FD:
+                self._nu = 0.0
+            elif getattr(self, "_nu_state", None) is not None:  # from the RHS pass
+                self._nu = D.global_norm(self._nu_state.read())[0]
+            else:
+                self._nu = D.norm2(self.u)[0]
         return self._nu
 
     @property

@@ -68,6 +68,24 @@ class StencilRhs:
                                C.c_void_p(out.data_ptr()), halo, D.stream()), "ek_rhs")
         return D.like_input(out, u)
 
+    def eval_with_norm(self, ud):
+        """(f(u), state block holding ||u||^2 of the local slab) in one pass
+        (ek_rhs_norm); device in, device out. Not charged: the caller
+        charges its counter."""
+        if ud.numel() != self.length:
+            raise ValueError(f"{self.name}: state length {ud.numel()} != {self.length}")
+        out = D.empty(self.length)
+        halo = None
+        if self.comm is not None:
+            hb = self.halo(ud)
+            halo = N.ptrs([hb, None, None])
+        st = D.scalar_state()
+        N.check(N.lib().ek_rhs_norm(C.byref(self.grid), C.c_void_p(ud.data_ptr()),
+                                    C.c_void_p(out.data_ptr()), st.ptr,
+                                    D.work_ptr(N.lib().ek_workspace_bytes(C.byref(self.grid))),
+                                    halo, D.stream()), "ek_rhs_norm")
+        return out, st
+
 
 class NativeJacFactory:
     """`jac_factory` of a problem with an exact Jacobian stencil: called with

@@ -161,7 +161,8 @@ def test_fused_leja_is_deterministic_and_matches_generic_path():
 def test_tma_and_register_kernels_agree(mk):
     """The TMA-staged 2-D kernels (row march, 32 x 8 chunks) / 3-D kernel and
     the register-staged ones agree bit for bit on every elementwise pass (RHS,
-    FD/analytic Jv, remainder); n = 600 / 520 give the row march interior
+    analytic Jv, remainder; FD ones within the FD tier, as they depend on the
+    linearisation's ||u||); n = 600 / 520 give the row march interior
     strips (no domain edge) as well as edge strips. Passes
     with a reduction (Leja, power iteration) partition the grid differently,
     so their norms differ in the last bit and the FD quotient amplifies that:
@@ -195,8 +196,16 @@ def test_tma_and_register_kernels_agree(mk):
     b, lb, rb = res[0]
     for mode in (1, 2, 3):
         a, la, ra = res[mode]
-        for x, y in zip(a, b):
-            assert np.array_equal(x, y), mode
+        assert np.array_equal(a[0], b[0]), mode          # f(u_n): bit-exact
+        # Jv / remainder: bit-exact for analytic Jacobians; with FD they go
+        # through ||u||, reduced in the RHS pass over this kernel's partition
+        # (last-ulp differences, amplified by the FD quotient: FD tier)
+        fd = p.jac_factory is None
+        for x, y in zip(a[1:], b[1:]):
+            if fd:
+                assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y), mode
+            else:
+                assert np.array_equal(x, y), mode
         assert abs(la - lb) <= 1e-12 * abs(lb)
         assert ra.iters == rb.iters and ra.freeze_iters == rb.freeze_iters
         for x, y in zip(ra.vectors, rb.vectors):
