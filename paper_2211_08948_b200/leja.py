@@ -191,13 +191,18 @@ def _slab_decide(st, Jn, table, base, m, k, begin):
 
 
 def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
-                              xi=None, max_points=DEFAULT_NUM_POINTS, _lazy_m0=False):
+                              xi=None, max_points=DEFAULT_NUM_POINTS, _lazy_m0=False,
+                              _first_batch=8):
     """phi_l(c_i h J) b for several scale factors c_i sharing one Newton
     basis recurrence (leja.py:133-189). Accumulator i freezes once
     |d_i[m]| ||y_m|| < tol; the loop runs until all are frozen.
 
     Returns LejaResult(vectors, iters, freeze_iters); raises NonConvergence
     after `max_points` terms or on a non-finite ||y||.
+
+    _first_batch: iterations enqueued before the first host check (the
+    engines pass the previous count of the same group + 1, so a call usually
+    needs one check; later iterations of a batch early-exit on the device).
 
     _lazy_m0 (integrator engines only, device b): if every accumulator
     freezes at m = 0 the results d_i[0]*b are returned as expressions
@@ -230,7 +235,12 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     if fused is not None and (fused[1] != 1.0 or fused[0].grid.problem == N.P_SEMILINEAR):
         fused = None
     Jn = fused[0] if fused else None
-    nu = Jn.nu if Jn is not None and Jn.jac == N.JAC_FD else 0.0
+    nu, nu_dev = 0.0, None
+    if Jn is not None and Jn.jac == N.JAC_FD:
+        if Jn._nu is None and getattr(Jn, "_nu_state", None) is not None and D.COMM is None:
+            nu_dev = Jn._nu_state  # ||u|| from the RHS pass: device copy, no host sync
+        else:
+            nu = Jn.nu
 
     slab = Jn is not None and Jn.comm is not None
     ps = [D.empty(n) for _ in range(k)]
@@ -240,6 +250,10 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     lazy = bool(_lazy_m0 and fold and isinstance(b, torch.Tensor))
     st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k, defer=1 if slab else 0,
                     p_init=-1 if fold else 0, lazy0=1 if lazy else 0)
+    if nu_dev is not None:
+        N.check(N.lib().ek_copy(C.c_void_p(st.buf.data_ptr() + N.LejaState.nu.offset),
+                                C.c_void_p(nu_dev.buf.data_ptr() + N.ScalarState.val.offset + 8),
+                                8, 3, D.stream()), "nu copy")
     ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(Jn.grid)) if Jn else None)
     pp = N.ptrs(ps)
     N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()), pp, k,
@@ -274,7 +288,7 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
         if Jn is not None:
             # launch batch: short first batch (most calls finish early), then
             # the rest of the chunk; kernels after termination early-exit
-            hi = min(m_avail, m + 8) if m == 1 else m_avail
+            hi = min(m_avail, m + max(1, int(_first_batch))) if m == 1 else m_avail
             if prof is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
