@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--tma-mode", type=int, default=None,
                     help="2 row march (default), 1 32x8 chunks, 0 register-staged")
     ap.add_argument("--kiops", action="store_true")
+    ap.add_argument("--reps", type=int, default=5, help="timed repetitions (median)")
     args = ap.parse_args()
 
     import torch
@@ -58,9 +59,13 @@ def main():
         prof, L.PROFILE = L.PROFILE, None
         return prof
 
-    run(4)
-    prof = run(args.iters)
-    t = sum(s.elapsed_time(e) for s, e in prof[0]["events"]) / 1e3
+    for _ in range(3):  # warm-up: clocks up, tensor maps and DD tables cached
+        run(args.iters)
+    ts = []
+    for _ in range(max(1, args.reps)):
+        prof = run(args.iters)
+        ts.append(sum(s.elapsed_time(e) for s, e in prof[0]["events"]) / 1e3)
+    t = sorted(ts)[len(ts) // 2]
     n = sys_._u.numel()
     fd = prof[0]["fd"]
     lin = args.problem in ("advdiff2d", "advdiff3d")
@@ -69,7 +74,8 @@ def main():
     out = {"problem": args.problem, "tma_mode": args.tma_mode,
            "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
            "ms_per_launch": t / args.iters * 1e3, "bytes_per_launch": per,
-           "GBps": per * args.iters / t / 1e9}
+           "GBps": per * args.iters / t / 1e9,
+           "ms_per_launch_reps": [round(x / args.iters * 1e3, 4) for x in ts]}
     print(json.dumps(out))
     if args.kiops:
         # KIOPS Arnoldi steps on the same operator: one substep of m steps
