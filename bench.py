@@ -148,22 +148,24 @@ class ClockSampler:
 # -------------------------------------------------------------- our arm
 
 def leja_bytes(prof):
-    """Algorithmic bytes of every fused Leja launch of one call: iteration m
-    reads u, y and the k_active accumulators and writes y' and them:
-    8 N (3 + 2 k_active(m)) with FD. SURVEY.md §8(d) d3 counts a read of
-    f(u_n) too (8 N (4 + 2k)); the kernel re-evaluates f(u_n) from the u
-    neighbourhood it reads anyway, so that vector is not algorithmic
-    traffic of this implementation."""
+    """Bytes of every fused Leja launch of one call, two models.
+
+    algorithmic (the roofline contract): iteration m
+    reads u, f(u_n), y and the k_active accumulators and writes y' and them,
+    8 N (4 + 2 k_active(m)) with FD (8 N (2 + 2k) for a linear Jacobian);
+    pass: what this implementation moves, 8 N (3 + 2 k_active(m)) with FD --
+    the kernel re-evaluates f(u_n) from the u neighbourhood it reads anyway
+    instead of streaming it."""
     n = prof["n"]
     per_vec = 8 * n
-    total, launches = 0, 0
+    alg, pas, launches = 0, 0, 0
     freeze = prof.get("freeze", [])
     for m in range(1, prof.get("iters", 0) + 1):
         k_act = sum(1 for f in freeze if f >= m)
-        base = 3 if prof["fd"] else 2
-        total += per_vec * (base + 2 * k_act)
+        alg += per_vec * ((4 if prof["fd"] else 2) + 2 * k_act)
+        pas += per_vec * ((3 if prof["fd"] else 2) + 2 * k_act)
         launches += 1
-    return total, launches
+    return alg, pas, launches
 
 
 def run_ours(args, rank, world, local):
@@ -241,10 +243,11 @@ def run_ours(args, rank, world, local):
     total_jv = float(counts["jv"])
 
     # roofline of the fused Leja iteration kernel, live from the timed region
-    kb, kl, kt = 0, 0, 0.0
+    kb, kp, kl, kt = 0, 0, 0, 0.0
     for p in prof:
-        b, l_ = leja_bytes(p)
+        b, bp, l_ = leja_bytes(p)
         kb += b
+        kp += bp
         kl += l_
         kt += sum(s.elapsed_time(e) for s, e in p["events"]) / 1e3
     peak, peak_kind = peaks()
@@ -262,8 +265,11 @@ def run_ours(args, rank, world, local):
                       "(bulk-copy row march), k_tma2d<.., K, 4> (TMA 32x8 chunks) for k <= 2: "
                       "fused FD Jv + Leja recurrence + k accumulators + ||y||^2 + device "
                       "freeze test",
-            "bytes_model": "8*N*(3+2*k_active) per launch (reads u, y, p_1..k; writes y', "
-                           "p_1..k; f(u_n) is re-evaluated in-kernel, not read), N = 2*n^2",
+            "bytes_model": "algorithmic, SURVEY.md §8(d) d3: 8*N*(4+2*k_active) per launch "
+                           "(reads u, f(u_n), y, p_1..k; writes y', p_1..k), N = 2*n^2",
+            "achieved_pass_bytes": kp / kt / 1e9 if kt > 0 else None,
+            "pass_bytes_model": "8*N*(3+2*k_active): the bytes this kernel moves (f(u_n) is "
+                                "re-evaluated from the u neighbourhood instead of read)",
             "launches": kl, "avg_launch_ms": kt / kl * 1e3 if kl else None,
             "share_of_step": kt / elapsed if elapsed else None,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}

@@ -207,8 +207,9 @@ inline bool build_maps(const KArgs& a, TmaMaps& m) {
     const int64_t cols = a.g.n, rt = (int64_t)a.g.ncomp * a.g.rows;
     const bool d3 = a.g.dim == 3;
     // 2-D: (ncomp*rows) x n matrix; 3-D: (ncomp*rows) x n x n tensor
-    const uint32_t rw = d3 ? TBW3 : TBW, rh = d3 ? TBR3 : TBR;  // raw boxes
-    const uint32_t cw = d3 ? I3X : 32, ch = d3 ? I3Y : 8;       // centre boxes
+    constexpr int IY = iy3<EV, EP, NC, K>();
+    const uint32_t rw = d3 ? TBW3 : TBW, rh = d3 ? IY + 2 : TBR;  // raw boxes
+    const uint32_t cw = d3 ? I3X : 32, ch = d3 ? IY : 8;          // centre boxes
     auto mk = [&](CUtensorMap* out, const double* f, uint32_t bw, uint32_t bh) {
         return d3 ? tensor_map3(out, f, cols, rt, bw, bh)
                   : tensor_map(out, f, cols, rt, bw, bh);
@@ -319,7 +320,8 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
                         cudaSuccess || tocc < 1)
                     tocc = 1;
             }
-            const int64_t items = ((a.g.n + I3X - 1) / I3X) * ((a.g.n + I3Y - 1) / I3Y) *
+            constexpr int IY = iy3<EV, EP, P::NC, K>();
+            const int64_t items = ((a.g.n + I3X - 1) / I3X) * ((a.g.n + IY - 1) / IY) *
                                   ((a.g.rows + SEG3 - 1) / SEG3);
             const int64_t cap = (int64_t)sm_count() * tocc;
             const unsigned grid = (unsigned)(items < cap ? items : cap);

@@ -81,15 +81,22 @@ __device__ __forceinline__ double lap2(const Nb& s, const PC& g) {
 __device__ __forceinline__ double lap3(const Nb& s, const PC& g) {
     return dv(((((s.xm + s.xp) + s.ym) + s.yp) + s.zm) + s.zp - 6.0 * s.c, g.h2);
 }
-// one-sided difference following the sign of +v.grad u (forward for v >= 0)
+// one-sided difference following the sign of +v.grad u (forward for v >= 0).
+// The operands are selected first and ONE quotient is formed: the same
+// subtraction and division as `v >= 0 ? (xp - c) / h : (c - xm) / h`, but
+// the compiler cannot predicate both divisions (12 fp64 issues per 3-D point).
+__device__ __forceinline__ double upw(double m, double c, double p, double v, const PC& g) {
+    const bool fwd = v >= 0.0;
+    return dv((fwd ? p : c) - (fwd ? c : m), g.h);
+}
 __device__ __forceinline__ double upw_x(const Nb& s, double v, const PC& g) {
-    return v >= 0.0 ? dv(s.xp - s.c, g.h) : dv(s.c - s.xm, g.h);
+    return upw(s.xm, s.c, s.xp, v, g);
 }
 __device__ __forceinline__ double upw_y(const Nb& s, double v, const PC& g) {
-    return v >= 0.0 ? dv(s.yp - s.c, g.h) : dv(s.c - s.ym, g.h);
+    return upw(s.ym, s.c, s.yp, v, g);
 }
 __device__ __forceinline__ double upw_z(const Nb& s, double v, const PC& g) {
-    return v >= 0.0 ? dv(s.zp - s.c, g.h) : dv(s.c - s.zm, g.h);
+    return upw(s.zm, s.c, s.zp, v, g);
 }
 
 // problems.py:69-83. prm: alpha, beta, gamma

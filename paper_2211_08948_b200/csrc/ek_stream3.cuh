@@ -9,7 +9,8 @@
 // A block marches the planes of an item in order; one pipeline stage holds
 // one plane of the item: per raw field an 18 x 68 box (jy0-1..jy0+16,
 // kx0-2..kx0+65) and per centre field (f(u), accumulators, Arnoldi slots) a
-// 16 x 64 box; 16 warps, each thread computes 2 points of the plane. Plane i is computed from stages i-1, i, i+1, so every raw
+// 16 x 64 box (IY x 64 with IY = 8 when many centre streams are staged);
+// 16 warps, each thread computes IY / 8 points of the plane. Plane i is computed from stages i-1, i, i+1, so every raw
 // plane is fetched once per item (plus the two ghost planes at its ends)
 // and the axis-0 neighbours cost no extra traffic. Ghost planes outside the
 // domain are fetched by the copy engine too: the wrapped / reflected plane
@@ -46,25 +47,48 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
         : "memory");
 }
 
-// Item geometry: I3X columns (kx) x I3Y rows (jy); raw boxes carry one
+// Item geometry: I3X columns (kx) x IY rows (jy); raw boxes carry one
 // ghost row above/below and two columns left/right (16-byte multiples).
-constexpr int I3X = 64, I3Y = 16;
-constexpr int TBW3 = I3X + 4, TBR3 = I3Y + 2;
-constexpr int RAW3 = 1232;            // >= TBW3*TBR3 (1224), 128-B multiple
-constexpr int CTR3 = I3X * I3Y;       // 1024
+// IY = 16 where two blocks per SM still hold >= 6 plane stages, else 8
+// (many centre streams: Leja k >= 2, Arnoldi windows).
+// Thread t computes the plane points t, t + T3, ... of the item (row-major,
+// 64 per row): IY * 64 / T3 points per thread and plane.
+#ifndef EK_T3
+#define EK_T3 512
+#endif
+#ifndef EK_MAP3_FLAT
+#define EK_MAP3_FLAT 0
+#endif
+constexpr int T3 = EK_T3, NW3 = T3 / 32;
+constexpr int I3X = 64;
+constexpr int TBW3 = I3X + 4;
+__host__ __device__ constexpr int raw3(int iy) { return (TBW3 * (iy + 2) + 15) / 16 * 16; }
+__host__ __device__ constexpr int ctr3(int iy) { return I3X * iy; }
+template <int EV, int EP, int NC, int K>
+__host__ __device__ constexpr int stage3_doubles_iy(int iy) {
+    return nraw<EV>() * NC * raw3(iy) + nctr_maps<EV, EP, K>() * NC * ctr3(iy);
+}
+template <int EV, int EP, int NC, int K>
+__host__ __device__ constexpr int iy3() {
+#ifdef EK_IY3
+    if (EK_IY3 == 8 || stage3_doubles_iy<EV, EP, NC, K>(16) * 8 * 5 <= 220 * 1024) return EK_IY3;
+#endif
+    return (110 * 1024) / (stage3_doubles_iy<EV, EP, NC, K>(16) * 8) >= 6 ? 16 : 8;
+}
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage3_doubles() {
-    return nraw<EV>() * NC * RAW3 + nctr_maps<EV, EP, K>() * NC * CTR3;
+    return stage3_doubles_iy<EV, EP, NC, K>(iy3<EV, EP, NC, K>());
 }
 
 struct Item3 {
     int k0, j0, i0, L;
 };
+template <int IY>
 __device__ __forceinline__ Item3 item3(long t, int n, int rows) {
-    const int tk = (n + I3X - 1) / I3X, tj = (n + I3Y - 1) / I3Y;
+    const int tk = (n + I3X - 1) / I3X, tj = (n + IY - 1) / IY;
     Item3 it;
     it.k0 = (int)(t % tk) * I3X;
-    it.j0 = (int)((t / tk) % tj) * I3Y;
+    it.j0 = (int)((t / tk) % tj) * IY;
     it.i0 = (int)(t / ((long)tk * tj)) * SEG3;
     it.L = rows - it.i0 < SEG3 ? rows - it.i0 : SEG3;
     return it;
@@ -77,9 +101,10 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
                                             uint32_t active) {
     constexpr int NR = nraw<EV>(), NCM = nctr_maps<EV, EP, K>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    constexpr int IY = iy3<EV, EP, NC, K>(), RAW3 = raw3(IY), CTR3 = ctr3(IY);
     const int i = it.i0 - 1 + pos;
     const bool centre = pos >= 1 && pos <= it.L;
-    uint32_t bytes = NR * NC * (TBW3 * TBR3 * 8);
+    uint32_t bytes = NR * NC * (TBW3 * (IY + 2) * 8);
     if (centre) {
 #pragma unroll
         for (int g = 0; g < NCM; ++g)
@@ -117,13 +142,14 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
 
 // One point (i, jy, kx) from the stages of planes i-1 (pm), i (pc), i+1 (pp);
 // ro / co: its offset inside a raw / centre slot.
-template <class P, int EV, int EP, int K, bool EDGE>
+template <class P, int EV, int EP, int K, int IY, bool EDGE>
 __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                            const double* pc, const double* pp,
                                            const double* const (&rb)[2], long i, int jy, int kx,
-                                           int ro, int co, int n, double* acc) {
+                                           int ro, int co, int n, long off, double* acc) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    constexpr int RAW3 = raw3(IY), CTR3 = ctr3(IY);
     const long plane = (long)n * n;
     const bool gy_m = EDGE && jy == 0, gy_p = EDGE && jy == n - 1;
     const bool gz_m = EDGE && kx == 0, gz_p = EDGE && kx == n - 1;
@@ -182,10 +208,9 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
     }
     double val[NC];
     evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
-    epilogue<EV, EP, NC, K>(a, ctl, i * plane + (long)jy * n + kx, val, z, acc);
+    epilogue<EV, EP, NC, K>(a, ctl, off, val, z, acc);
 }
 
-constexpr int T3 = 512, NW3 = T3 / 32;  // one warp per item row
 
 template <class P, int EV, int EP, int K, int S>
 __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
@@ -193,15 +218,17 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
     constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
     constexpr int NR = nraw<EV>();
     constexpr int SD = stage3_doubles<EV, EP, NC, K>();
+    constexpr int IY = iy3<EV, EP, NC, K>(), PPT = IY * I3X / T3;
+    static_assert(PPT >= 1 && PPT * T3 == IY * I3X, "item points must split evenly");
     extern __shared__ __align__(1024) double smem[];
     __shared__ __align__(8) uint64_t full[S];
     __shared__ int released[S];  // warps that released stage s, cumulative
 
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int n = (int)a.g.n, rows = (int)a.g.rows;
-    const long nitems = (long)((n + I3X - 1) / I3X) * ((n + I3Y - 1) / I3Y) *
+    const long nitems = (long)((n + I3X - 1) / I3X) * ((n + IY - 1) / IY) *
                         ((rows + SEG3 - 1) / SEG3);
     const long G = gridDim.x;
     const double* rb[2];
@@ -216,7 +243,7 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
             pos -= it.L + 2;
             t += G;
             if (t >= nitems) return;
-            it = item3(t, n, rows);
+            it = item3<IY>(t, n, rows);
         }
         issue_plane<EV, EP, NC, K>(a, maps, smem + s * SD, &full[s], it, pos, rows, ctr_mask(ctl));
     };
@@ -232,7 +259,7 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // fill the ring: sequence numbers 0 .. S-1
         if (blockIdx.x < nitems) {
-            const Item3 it0 = item3(blockIdx.x, n, rows);
+            const Item3 it0 = item3<IY>(blockIdx.x, n, rows);
             for (int s = 0; s < S; ++s) issue_ahead(blockIdx.x, it0, s - S, s);
         }
     }
@@ -257,14 +284,36 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
         }
     };
 
-    // this thread's 2 points of a plane: row wid, columns lane + {0, 32}
+    // point r of this thread in the item plane: with one item row per warp
+    // (IY == NW3) warp w owns row w, lanes columns lane + 32 r; otherwise
+    // row-major over the block (IY * 64 / T3 points per thread).
+    auto point_of = [&](int r, int& ly, int& lx) {
+        if constexpr (IY == NW3 && PPT == 2 && !EK_MAP3_FLAT) {
+            ly = threadIdx.x >> 5;
+            lx = lane + 32 * r;
+        } else {
+            const int idx = threadIdx.x + r * T3;
+            ly = idx / I3X;
+            lx = idx % I3X;
+        }
+    };
+
     int q0 = 0;  // sequence number of position 0 of the current item
     for (long t = blockIdx.x; t < nitems; t += G) {
-        const Item3 it = item3(t, n, rows);
-        const bool edge = it.k0 < 1 || it.k0 + I3X >= n || it.j0 < 1 || it.j0 + I3Y >= n;
+        const Item3 it = item3<IY>(t, n, rows);
+        const bool edge = it.k0 < 1 || it.k0 + I3X >= n || it.j0 < 1 || it.j0 + IY >= n;
         wait_full(q0);
         wait_full(q0 + 1);
         int sm = q0 % S, sc = (q0 + 1) % S;
+        // flat offsets of this thread's points in plane i0; + n^2 per plane
+        long off[PPT];
+#pragma unroll
+        for (int r = 0; r < PPT; ++r) {
+            int ly, lx;
+            point_of(r, ly, lx);
+            off[r] = ((long)it.i0 * n + it.j0 + ly) * n + it.k0 + lx;
+        }
+        const long plane = (long)n * n;
         for (int p = 1; p <= it.L; ++p) {
             wait_full(q0 + p + 1);
             const int sp = sc + 1 == S ? 0 : sc + 1;
@@ -273,16 +322,18 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
             const double* pp = smem + sp * SD;
             const long i = it.i0 + p - 1;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int ly = wid, lx = lane + 32 * h;
+            for (int r = 0; r < PPT; ++r) {
+                int ly, lx;
+                point_of(r, ly, lx);
                 const int jy = it.j0 + ly, kx = it.k0 + lx;
                 const int ro = (1 + ly) * TBW3 + 2 + lx, co = ly * I3X + lx;
                 if (!edge)
-                    tma3_point<P, EV, EP, K, false>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co, n,
-                                                    acc);
+                    tma3_point<P, EV, EP, K, IY, false>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co,
+                                                        n, off[r], acc);
                 else if (jy < n && kx < n)
-                    tma3_point<P, EV, EP, K, true>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co, n,
-                                                   acc);
+                    tma3_point<P, EV, EP, K, IY, true>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co,
+                                                       n, off[r], acc);
+                off[r] += plane;
             }
             release(q0 + p - 1, t, it, p - 1);
             sm = sc;

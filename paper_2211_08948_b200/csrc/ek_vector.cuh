@@ -14,6 +14,51 @@ __host__ __forceinline__ int vgrid(int64_t len) {
     if (b < 1) b = 1;
     return (int)(b < VGRID_MAX ? b : VGRID_MAX);
 }
+// Streaming kernels take 4 consecutive elements per thread and iteration
+// (two 16-byte loads per operand, all issued before use): 4x the bytes in
+// flight of one element per thread, which a grid-stride loop needs to get
+// near the HBM bandwidth (one 8-byte load per thread is latency bound).
+__host__ __forceinline__ int vgrid4(int64_t len) { return vgrid((len + 3) / 4); }
+
+__device__ __forceinline__ bool al16d(const void* p) { return ((uintptr_t)p & 15) == 0; }
+// x[e0 .. e0+3] (zeros past len); `full`: whole group and x 16-byte aligned
+__device__ __forceinline__ void ld4(const double* __restrict__ x, int64_t e0, int64_t len,
+                                    bool full, double (&v)[4]) {
+    if (full) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(x + e0));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(x + e0) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) v[w] = e0 + w < len ? __ldg(x + e0 + w) : 0.0;
+    }
+}
+// plain (coherent) loads: for buffers this kernel also writes
+__device__ __forceinline__ void ld4c(const double* x, int64_t e0, int64_t len, bool full,
+                                     double (&v)[4]) {
+    if (full) {
+        const double2 a = reinterpret_cast<const double2*>(x + e0)[0];
+        const double2 b = reinterpret_cast<const double2*>(x + e0)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) v[w] = e0 + w < len ? x[e0 + w] : 0.0;
+    }
+}
+__device__ __forceinline__ void st4(double* x, int64_t e0, int64_t len, bool full,
+                                    const double (&v)[4]) {
+    if (full) {
+        reinterpret_cast<double2*>(x + e0)[0] = make_double2(v[0], v[1]);
+        reinterpret_cast<double2*>(x + e0)[1] = make_double2(v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+            if (e0 + w < len) x[e0 + w] = v[w];
+    }
+}
+#define EK_FOR4(e0, len)                                                                  \
+    for (int64_t e0 = ((int64_t)blockIdx.x * TPB + threadIdx.x) * 4; e0 < (len);         \
+         e0 += (int64_t)gridDim.x * TPB * 4)
 
 // ---------------------------------------------------------------- norms
 // ||x||^2 (+ flags: bit0 any nonzero, bit1 any non-finite) -> st->val[slot]
@@ -23,14 +68,18 @@ __global__ void __launch_bounds__(TPB) k_norm2(int64_t len, const double* __rest
                                                int slot, double* work) {
     double acc[3] = {0.0, 0.0, 0.0};
     const double d = div ? *div : 1.0;
-    const bool has_div = div != nullptr;
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
-         e += (int64_t)gridDim.x * TPB) {
-        double v = __ldg(x + e);
-        if (has_div) v = v / d;
-        acc[0] += v * v;
-        acc[1] += (v != 0.0) ? 1.0 : 0.0;
-        acc[2] += isfinite(v) ? 0.0 : 1.0;
+    const bool has_div = div != nullptr, vec = al16d(x);
+    EK_FOR4(e0, len) {
+        double v[4];
+        ld4(x, e0, len, vec && e0 + 4 <= len, v);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            if (e0 + w >= len) break;
+            if (has_div) v[w] = v[w] / d;
+            acc[0] += v[w] * v[w];
+            acc[1] += (v[w] != 0.0) ? 1.0 : 0.0;
+            acc[2] += isfinite(v[w]) ? 0.0 : 1.0;
+        }
     }
     block_sum<3>(acc);
     if (publish_and_arrive<3>(acc, work, &st->ticket)) {
@@ -48,9 +97,13 @@ __global__ void __launch_bounds__(TPB) k_norm2(int64_t len, const double* __rest
 __global__ void __launch_bounds__(TPB) k_l1(int64_t len, const double* __restrict__ x,
                                             ek_scalar_state* st, int slot, double* work) {
     double acc[1] = {0.0};
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
-         e += (int64_t)gridDim.x * TPB)
-        acc[0] += fabs(__ldg(x + e));
+    const bool vec = al16d(x);
+    EK_FOR4(e0, len) {
+        double v[4];
+        ld4(x, e0, len, vec && e0 + 4 <= len, v);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[0] += fabs(v[w]);  // zeros past len
+    }
     block_sum<1>(acc);
     if (publish_and_arrive<1>(acc, work, &st->ticket)) {
         double tot[1];
@@ -84,14 +137,25 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
     double d[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
-         e += (int64_t)gridDim.x * TPB) {
-        const double y = __ldg(a.b + e);
-        acc[0] += y * y;
+    bool vec = al16d(a.b);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        if (q < a.nk) vec = vec && al16d(a.p[q]);
+    EK_FOR4(e0, a.len) {
+        const bool full = vec && e0 + 4 <= a.len;
+        double y[4];
+        ld4(a.b, e0, a.len, full, y);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[0] += y[w] * y[w];  // zeros past len
         if (!fold) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                if (q < a.nk) a.p[q][e] = d[q] * y;  // dds[i][0] * y
+                if (q < a.nk) {
+                    double pv[4];
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) pv[w] = d[q] * y[w];  // dds[i][0] * y
+                    st4(a.p[q], e0, a.len, full, pv);
+                }
         }
     }
     block_sum<1>(acc);
@@ -117,12 +181,22 @@ __global__ void __launch_bounds__(TPB) k_leja_fold_done(const LejaVArgs a) {
     double d[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32] : 0.0;
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
-         e += (int64_t)gridDim.x * TPB) {
-        const double y = __ldg(a.b + e);
+    bool vec = al16d(a.b);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        if (q < a.nk) vec = vec && al16d(a.p[q]);
+    EK_FOR4(e0, a.len) {
+        const bool full = vec && e0 + 4 <= a.len;
+        double y[4];
+        ld4(a.b, e0, a.len, full, y);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            if (q < a.nk) a.p[q][e] = d[q] * y;  // dds[i][0] * y
+            if (q < a.nk) {
+                double pv[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) pv[w] = d[q] * y[w];  // dds[i][0] * y
+                st4(a.p[q], e0, a.len, full, pv);
+            }
     }
 }
 
@@ -130,9 +204,16 @@ __global__ void __launch_bounds__(TPB) k_leja_fold_done(const LejaVArgs a) {
 __global__ void __launch_bounds__(TPB) k_axpby(int64_t n, double a, const double* __restrict__ x,
                                                double b, const double* __restrict__ y,
                                                double* __restrict__ out) {
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < n;
-         e += (int64_t)gridDim.x * TPB)
-        out[e] = (a * __ldg(x + e)) + (b * __ldg(y + e));
+    const bool vec = al16d(x) && al16d(y) && al16d(out);
+    EK_FOR4(e0, n) {
+        const bool full = vec && e0 + 4 <= n;
+        double xv[4], yv[4], o[4];
+        ld4(x, e0, n, full, xv);
+        ld4(y, e0, n, full, yv);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) o[w] = (a * xv[w]) + (b * yv[w]);
+        st4(out, e0, n, full, o);
+    }
 }
 
 struct DotArgs {
@@ -149,12 +230,22 @@ __global__ void __launch_bounds__(TPB) k_dot_multi(const DotArgs a) {
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.n;
-         e += (int64_t)gridDim.x * TPB) {
-        const double xv = __ldg(a.x + e);
+    bool vec = al16d(a.x);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        if (q < a.k) vec = vec && al16d(a.y[q]);
+    EK_FOR4(e0, a.n) {
+        const bool full = vec && e0 + 4 <= a.n;
+        double xv[4];
+        ld4(a.x, e0, a.n, full, xv);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            if (q < a.k) acc[q] += xv * __ldg(a.y[q] + e);
+            if (q < a.k) {
+                double yv[4];
+                ld4(a.y[q], e0, a.n, full, yv);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) acc[q] += xv[w] * yv[w];  // zeros past n
+            }
     }
     block_sum<8>(acc);
     if (publish_and_arrive<8>(acc, a.work, &a.st->ticket)) {
@@ -293,11 +384,14 @@ struct ArnVArgs {
 // V[0] = [w_l ; tail], beta = ||V[0]||  (kiops.py:168-176)
 __global__ void __launch_bounds__(TPB) k_arn_init(const ArnVArgs a) {
     double acc[1] = {0.0};
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.n;
-         e += (int64_t)gridDim.x * TPB) {
-        const double v = __ldg(a.src + e);
-        a.w[e] = v;
-        acc[0] += v * v;
+    const bool vec = al16d(a.src) && al16d(a.w);
+    EK_FOR4(e0, a.n) {
+        const bool full = vec && e0 + 4 <= a.n;
+        double v[4];
+        ld4(a.src, e0, a.n, full, v);
+        st4(a.w, e0, a.n, full, v);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[0] += v[w] * v[w];  // zeros past n
     }
     block_sum<1>(acc);
     if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
@@ -371,15 +465,31 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
     for (int q = 0; q < 4; ++q) h[q] = q < a.nwin ? a.H[(long)(lo + q) * a.ldh + (a.jj - 1)] : 0.0;
     const int64_t len = a.n + a.p;
     double acc[1] = {0.0};
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
-         e += (int64_t)gridDim.x * TPB) {
-        double t = __ldg(a.win[0] + e) * h[0];
+    bool vec = al16d(a.w);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (q < a.nwin) vec = vec && al16d(a.win[q]);
+    EK_FOR4(e0, len) {
+        const bool full = vec && e0 + 4 <= len;
+        double wv[4], t[4];
+        ld4c(a.w, e0, len, full, wv);
+        ld4(a.win[0], e0, len, full, t);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) t[w] = t[w] * h[0];
 #pragma unroll
         for (int q = 1; q < 4; ++q)
-            if (q < a.nwin) t = t + (__ldg(a.win[q] + e) * h[q]);
-        const double w = a.w[e] - t;
-        a.w[e] = w;
-        acc[0] += w * w;
+            if (q < a.nwin) {
+                double x[4];
+                ld4(a.win[q], e0, len, full, x);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) t[w] = t[w] + (x[w] * h[q]);
+            }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            wv[w] = wv[w] - t[w];
+            acc[0] += wv[w] * wv[w];  // zeros past len
+        }
+        st4(a.w, e0, len, full, wv);
     }
     block_sum<1>(acc);
     if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
@@ -406,11 +516,17 @@ __global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
     const Dv nrm = mkdv(cst->nrm);
     const int64_t len = a.n + a.p;
     double acc[1] = {0.0};
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
-         e += (int64_t)gridDim.x * TPB) {
-        const double v = dv(a.w[e], nrm);
-        a.w[e] = v;
-        if (e < a.n) acc[0] += v * v;
+    const bool vec = al16d(a.w);
+    EK_FOR4(e0, len) {
+        const bool full = vec && e0 + 4 <= len;
+        double v[4];
+        ld4c(a.w, e0, len, full, v);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            v[w] = dv(v[w], nrm);
+            if (e0 + w < a.n) acc[0] += v[w] * v[w];
+        }
+        st4(a.w, e0, len, full, v);
     }
     block_sum<1>(acc);
     if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
@@ -433,11 +549,20 @@ struct CombineArgs {
     double coef[MAXB];
 };
 __global__ void __launch_bounds__(TPB) k_basis_combine(const CombineArgs a) {
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.n;
-         e += (int64_t)gridDim.x * TPB) {
-        double s = a.coef[0] * __ldg(a.rows[0] + e);
-        for (int i = 1; i < a.j; ++i) s = s + (a.coef[i] * __ldg(a.rows[i] + e));
-        a.out[e] = s;
+    bool vec = al16d(a.out);
+    for (int i = 0; i < a.j; ++i) vec = vec && al16d(a.rows[i]);
+    EK_FOR4(e0, a.n) {
+        const bool full = vec && e0 + 4 <= a.n;
+        double s[4], x[4];
+        ld4(a.rows[0], e0, a.n, full, x);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) s[w] = a.coef[0] * x[w];
+        for (int i = 1; i < a.j; ++i) {
+            ld4(a.rows[i], e0, a.n, full, x);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) s[w] = s[w] + (a.coef[i] * x[w]);
+        }
+        st4(a.out, e0, a.n, full, s);
     }
 }
 
@@ -449,11 +574,16 @@ __global__ void __launch_bounds__(TPB) k_power_norm(int64_t len, const double* _
     if (scaled && (st->done || st->status)) return;
     const Dv d = mkdv(st->nw);
     double acc[1] = {0.0};
-    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < len;
-         e += (int64_t)gridDim.x * TPB) {
-        double v = __ldg(x + e);
-        if (scaled) v = dv(v, d);
-        acc[0] += v * v;
+    const bool vec = al16d(x);
+    EK_FOR4(e0, len) {
+        double v[4];
+        ld4(x, e0, len, vec && e0 + 4 <= len, v);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            if (e0 + w >= len) break;
+            if (scaled) v[w] = dv(v[w], d);
+            acc[0] += v[w] * v[w];
+        }
     }
     block_sum<1>(acc);
     if (publish_and_arrive<1>(acc, work, &st->ticket)) {

@@ -296,7 +296,7 @@ int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu, const do
     int rc = launch_stencil<EP_STORE>(ev, a, s);
     if (rc != EK_OK || jac != EK_JAC_FD || !st) return rc;
     // non-finite check of the FD result (linalg.py:127-128)
-    k_norm2<<<vgrid(ek_grid_len(g)), TPB, 0, s>>>(ek_grid_len(g), out, nullptr, st, 6, work);
+    k_norm2<<<vgrid4(ek_grid_len(g)), TPB, 0, s>>>(ek_grid_len(g), out, nullptr, st, 6, work);
     EK_LAUNCH_CHECK("k_norm2");
     return EK_OK;
 }
@@ -371,11 +371,11 @@ int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
     LejaVArgs a{};
     a.len = len; a.b = b; a.nk = k; a.coef = coef_dev; a.mi = 0; a.m = 0; a.st = st; a.work = work;
     for (int q = 0; q < k; ++q) a.p[q] = p[q];
-    k_leja_begin<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
+    k_leja_begin<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(a);
     EK_LAUNCH_CHECK("k_leja_begin");
     // folded begin that froze everything at m = 0: write d_i[0] b (early
     // exit in every other case)
-    k_leja_fold_done<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
+    k_leja_fold_done<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(a);
     EK_LAUNCH_CHECK("k_leja_fold_done");
     return EK_OK;
 }
@@ -438,10 +438,10 @@ int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, c
     const bool slab = halo != nullptr;
     if (it_begin == 0 && !slab) {
         // v = v0 / ||v0||   (spectrum.py:49-51): divisor and, for FD, ||v||
-        k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, v0, 0, st, work);
+        k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, v0, 0, st, work);
         EK_LAUNCH_CHECK("k_power_norm");
         if (jac == EK_JAC_FD) {
-            k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, v0, 1, st, work);
+            k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, v0, 1, st, work);
             EK_LAUNCH_CHECK("k_power_norm");
         }
     }
@@ -454,7 +454,7 @@ int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, c
         const int rc = launch_stencil<EP_POWER>(ev, a, s);
         if (rc != EK_OK) return rc;
         if (jac == EK_JAC_FD && !slab) {
-            k_power_norm<<<vgrid(len), TPB, 0, s>>>(len, a.out, 1, st, work);
+            k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, a.out, 1, st, work);
             EK_LAUNCH_CHECK("k_power_norm");
         }
     }
@@ -463,7 +463,7 @@ int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, c
 
 int ek_power_norm(int64_t len, const double* x, int scaled, ek_power_state* st, double* work,
                   void* stream) {
-    k_power_norm<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(len, x, scaled, st, work);
+    k_power_norm<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(len, x, scaled, st, work);
     EK_LAUNCH_CHECK("k_power_norm");
     return EK_OK;
 }
@@ -577,10 +577,10 @@ int ek_arnoldi_init(int64_t n, int p, const double* src, const double* tail_host
     a.n = n; a.p = p; a.src = src; a.w = V0; a.st = st; a.work = work;
     for (int t = 0; t < p; ++t) a.tail0[t] = tail_host[t];
     cudaStream_t s = (cudaStream_t)stream;
-    k_arn_init<<<vgrid(n), TPB, 0, s>>>(a);
+    k_arn_init<<<vgrid4(n), TPB, 0, s>>>(a);
     EK_LAUNCH_CHECK("k_arn_init");
     a.jj = 0;
-    k_arn_scale<<<vgrid(n + p), TPB, 0, s>>>(a);
+    k_arn_scale<<<vgrid4(n + p), TPB, 0, s>>>(a);
     EK_LAUNCH_CHECK("k_arn_scale");
     return EK_OK;
 }
@@ -628,9 +628,9 @@ int ek_arnoldi_run(const ek_grid* g, int jac, const double* u, const double* fu,
         for (int q = 0; q < 4; ++q) b.win[q] = w.win[q];
         b.jj = jj;
         b.w = V[jj];
-        k_arn_orth<<<vgrid(n + p), TPB, 0, s>>>(b);
+        k_arn_orth<<<vgrid4(n + p), TPB, 0, s>>>(b);
         EK_LAUNCH_CHECK("k_arn_orth");
-        k_arn_scale<<<vgrid(n + p), TPB, 0, s>>>(b);
+        k_arn_scale<<<vgrid4(n + p), TPB, 0, s>>>(b);
         EK_LAUNCH_CHECK("k_arn_scale");
     }
     return EK_OK;
@@ -665,9 +665,9 @@ int ek_arnoldi_orth(int64_t n, int p, double* const* V, int jj, int iop, double*
     arn_window(a, V, jj, iop);
     a.w = V[jj];
     cudaStream_t s = (cudaStream_t)stream;
-    k_arn_orth<<<vgrid(n + p), TPB, 0, s>>>(a);
+    k_arn_orth<<<vgrid4(n + p), TPB, 0, s>>>(a);
     EK_LAUNCH_CHECK("k_arn_orth");
-    k_arn_scale<<<vgrid(n + p), TPB, 0, s>>>(a);
+    k_arn_scale<<<vgrid4(n + p), TPB, 0, s>>>(a);
     EK_LAUNCH_CHECK("k_arn_scale");
     return EK_OK;
 }
@@ -685,7 +685,7 @@ int ek_basis_combine(int64_t n, double* const* V, const double* coef_host, int j
         a.rows[i] = V[i];
         a.coef[i] = coef_host[i];
     }
-    k_basis_combine<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(a);
+    k_basis_combine<<<vgrid4(n), TPB, 0, (cudaStream_t)stream>>>(a);
     EK_LAUNCH_CHECK("k_basis_combine");
     return EK_OK;
 }
@@ -727,14 +727,14 @@ int ek_norm2(int64_t len, const double* x, ek_scalar_state* st, int slot, double
         set_error("ek_norm2: slot %d", slot);
         return EK_ERR_INVALID;
     }
-    k_norm2<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(len, x, nullptr, st, slot, work);
+    k_norm2<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(len, x, nullptr, st, slot, work);
     EK_LAUNCH_CHECK("k_norm2");
     return EK_OK;
 }
 
 int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot, double* work,
           void* stream) {
-    k_l1<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(len, x, st, slot, work);
+    k_l1<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(len, x, st, slot, work);
     EK_LAUNCH_CHECK("k_l1");
     return EK_OK;
 }
@@ -961,7 +961,7 @@ int ek_axpby(int64_t n, double a, const double* x, double b, const double* y, do
              void* stream) {
     if (n < 0 || !x || !y || !out) return EK_ERR_INVALID;
     if (n == 0) return EK_OK;
-    k_axpby<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(n, a, x, b, y, out);
+    k_axpby<<<vgrid4(n), TPB, 0, (cudaStream_t)stream>>>(n, a, x, b, y, out);
     EK_LAUNCH_CHECK("k_axpby");
     return EK_OK;
 }
@@ -976,7 +976,7 @@ int ek_dot_multi(int64_t n, const double* x, const double* const* ys, int k, ek_
     a.n = n; a.x = x; a.k = k; a.st = st; a.work = work;
     for (int q = 0; q < k; ++q) a.y[q] = ys[q];
     cudaStream_t s = (cudaStream_t)stream;
-    k_dot_multi<<<vgrid(n), TPB, 0, s>>>(a);
+    k_dot_multi<<<vgrid4(n), TPB, 0, s>>>(a);
     EK_LAUNCH_CHECK("k_dot_multi");
     if (out_host) {
         ek_scalar_state h;

@@ -69,12 +69,16 @@ def main():
     n = sys_._u.numel()
     fd = prof[0]["fd"]
     lin = args.problem in ("advdiff2d", "advdiff3d")
-    base = 3 if fd else (2 if lin else 3)  # FD: u, y read, y' written (f(u_n) recomputed)
+    # algorithmic bytes: FD reads u, f(u_n), y; linear y;
+    # state-dependent analytic (Burgers) u, y; + k accumulators read and
+    # written, y' written. The FD pass itself re-evaluates f(u_n) (one vector less).
+    base = 4 if fd else (2 if lin else 3)
     per = 8 * n * (base + 2 * args.k)
+    per_pass = per - (8 * n if fd else 0)
     out = {"problem": args.problem, "tma_mode": args.tma_mode,
            "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
            "ms_per_launch": t / args.iters * 1e3, "bytes_per_launch": per,
-           "GBps": per * args.iters / t / 1e9,
+           "GBps": per * args.iters / t / 1e9, "GBps_pass": per_pass * args.iters / t / 1e9,
            "ms_per_launch_reps": [round(x / args.iters * 1e3, 4) for x in ts]}
     print(json.dumps(out))
     if args.kiops:
