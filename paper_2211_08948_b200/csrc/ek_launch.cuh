@@ -104,12 +104,20 @@ constexpr int tma_stages2() {
 }
 
 // 3-D plane ring: i-1, i, i+1 resident plus S-3 planes in flight; two
-// blocks per SM if that leaves >= 5 stages, else one (0: no TMA variant).
+// blocks per SM if 5 stages fit, else one (0: no TMA variant).
 template <int EV, int EP, int NC, int K>
 constexpr int tma_stages3() {
     constexpr int bytes = stage3_doubles<EV, EP, NC, K>() * 8;
     constexpr int two = (110 * 1024) / bytes, one = (220 * 1024) / bytes;
-    return two >= 5 ? (two > 12 ? 12 : two) : (one >= 5 ? (one > 12 ? 12 : one) : 0);
+#ifdef EK_S3
+    if (EK_S3 > 0 && EK_S3 * bytes <= (EK_LB3 == 1 ? 220 : 110) * 1024) return EK_S3;
+#endif
+    if (EK_LB3 == 1) return one >= 5 ? (one > 16 ? 16 : one) : 0;
+    // 5 stages (i-1, i, i+1 resident, two planes in flight) measured best on
+    // the B200 for k = 1..3 at 512^3 (1.04 / 1.45 / 1.77 ms vs 1.06 / 1.57 /
+    // 1.97 ms with 6 and 1.43 / 1.71 / 1.89 ms with 4): a deeper ring leaves
+    // less L1 for the boundary items' ghost loads and the spill slots.
+    return two >= 5 ? 5 : (one >= 5 ? 5 : 0);
 }
 
 // ---- tensor maps (driver entry point through the runtime, cached)
@@ -224,6 +232,10 @@ inline bool build_maps(const KArgs& a, TmaMaps& m) {
     int t = 0;
     for (int f = 0; f < nraw<EV>(); ++f) {
         if (!mk(&m.m[t++], raw[f], rw, rh)) return false;
+        // 3-D ghost side slots (boundary items): one row, one column pair
+        if (d3 && (!tensor_map3(&m.gr[f], raw[f], cols, rt, TBW3, 1) ||
+                   !tensor_map3(&m.gc[f], raw[f], cols, rt, 2, IY + 2)))
+            return false;
         if (d3 && a.g.slab &&
             (!hal[f] || !al16(hal[f]) ||
              !tensor_map3(&m.h[f], hal[f], cols, 2 * (int64_t)a.g.ncomp, rw, rh)))

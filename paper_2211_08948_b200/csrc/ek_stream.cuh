@@ -41,6 +41,8 @@ constexpr int MAX_MAPS = 11;     // 2 raw + f(u) + 8 accumulators
 struct TmaMaps {
     CUtensorMap m[MAX_MAPS];     // [0, nraw) raw fields, then f(u), then p_q
     CUtensorMap h[2];            // 3-D slab: halo buffers of the raw fields
+    CUtensorMap gr[2];           // 3-D: one ghost row (box TBW3 x 1) of a raw field
+    CUtensorMap gc[2];           // 3-D: one ghost column pair (box 2 x (IY+2)) of a raw field
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

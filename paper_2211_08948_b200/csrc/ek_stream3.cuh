@@ -56,6 +56,9 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
 #ifndef EK_T3
 #define EK_T3 512
 #endif
+#ifndef EK_LB3
+#define EK_LB3 2  // resident blocks per SM the register budget is sized for
+#endif
 #ifndef EK_MAP3_FLAT
 #define EK_MAP3_FLAT 0
 #endif
@@ -64,16 +67,22 @@ constexpr int I3X = 64;
 constexpr int TBW3 = I3X + 4;
 __host__ __device__ constexpr int raw3(int iy) { return (TBW3 * (iy + 2) + 15) / 16 * 16; }
 __host__ __device__ constexpr int ctr3(int iy) { return I3X * iy; }
+// Ghost side slots of a raw field (boundary items only): the wrapped /
+// reflected row above (j = -1) and below (j = n), TBW3 wide, and the ghost
+// column pair left (k = -1) and right (k = n), IY + 2 rows; 128-B multiples.
+constexpr int GROW3 = 80;  // >= TBW3
+__host__ __device__ constexpr int gcol3(int iy) { return (2 * (iy + 2) + 15) / 16 * 16; }
+__host__ __device__ constexpr int side3(int iy) { return 2 * GROW3 + 2 * gcol3(iy); }
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage3_doubles_iy(int iy) {
-    return nraw<EV>() * NC * raw3(iy) + nctr_maps<EV, EP, K>() * NC * ctr3(iy);
+    return nraw<EV>() * NC * (raw3(iy) + side3(iy)) + nctr_maps<EV, EP, K>() * NC * ctr3(iy);
 }
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int iy3() {
 #ifdef EK_IY3
     if (EK_IY3 == 8 || stage3_doubles_iy<EV, EP, NC, K>(16) * 8 * 5 <= 220 * 1024) return EK_IY3;
 #endif
-    return (110 * 1024) / (stage3_doubles_iy<EV, EP, NC, K>(16) * 8) >= 6 ? 16 : 8;
+    return (110 * 1024) / (stage3_doubles_iy<EV, EP, NC, K>(16) * 8) >= 5 ? 16 : 8;
 }
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage3_doubles() {
@@ -104,7 +113,13 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
     constexpr int IY = iy3<EV, EP, NC, K>(), RAW3 = raw3(IY), CTR3 = ctr3(IY);
     const int i = it.i0 - 1 + pos;
     const bool centre = pos >= 1 && pos <= it.L;
+    const int n = (int)a.g.n;
+    // ghost sides needed by this item's points (centre planes only)
+    const bool gym = centre && it.j0 == 0, gyp = centre && it.j0 + IY >= n;
+    const bool gzm = centre && it.k0 == 0, gzp = centre && it.k0 + I3X >= n;
     uint32_t bytes = NR * NC * (TBW3 * (IY + 2) * 8);
+    bytes += NR * NC * (((gym ? 1 : 0) + (gyp ? 1 : 0)) * TBW3 * 8 +
+                        ((gzm ? 1 : 0) + (gzp ? 1 : 0)) * 2 * (IY + 2) * 8);
     if (centre) {
 #pragma unroll
         for (int g = 0; g < NCM; ++g)
@@ -125,6 +140,16 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
                 const int w = (int)wrap_idx(i, rows, a.g.bc);
                 tma_load_3d(dst, &maps.m[f], it.k0 - 2, it.j0 - 1, c * rows + w, bar);
             }
+            double* sd = buf + NR * NC * RAW3 + NCM * NC * CTR3 + (f * NC + c) * side3(IY);
+            const int z = c * rows + i;
+            if (gym) tma_load_3d(sd, &maps.gr[f], it.k0 - 2, (int)wrap_idx(-1, n, a.g.bc), z, bar);
+            if (gyp) tma_load_3d(sd + GROW3, &maps.gr[f], it.k0 - 2, (int)wrap_idx(n, n, a.g.bc), z, bar);
+            // column pair boxes start on an even column (16-byte aligned box
+            // origin); the ghost is element (column & 1) of each box row
+            if (gzm) tma_load_3d(sd + 2 * GROW3, &maps.gc[f], (int)wrap_idx(-1, n, a.g.bc) & ~1,
+                                 it.j0 - 1, z, bar);
+            if (gzp) tma_load_3d(sd + 2 * GROW3 + gcol3(IY), &maps.gc[f],
+                                 (int)wrap_idx(n, n, a.g.bc) & ~1, it.j0 - 1, z, bar);
         }
     if (centre) {
         double* ctr = buf + NR * NC * RAW3;
@@ -145,12 +170,12 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
 template <class P, int EV, int EP, int K, int IY, bool EDGE>
 __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                            const double* pc, const double* pp,
-                                           const double* const (&rb)[2], long i, int jy, int kx,
-                                           int ro, int co, int n, long off, double* acc) {
+                                           int ly, int lx, int jy, int kx, int ro, int co, int n,
+                                           long off, double* acc) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     constexpr int RAW3 = raw3(IY), CTR3 = ctr3(IY);
-    const long plane = (long)n * n;
+    constexpr int SIDE = NR * NC * RAW3 + nctr_maps<EV, EP, K>() * NC * CTR3;
     const bool gy_m = EDGE && jy == 0, gy_p = EDGE && jy == n - 1;
     const bool gz_m = EDGE && kx == 0, gz_p = EDGE && kx == n - 1;
     Nb nb[NC][NCH];
@@ -166,11 +191,15 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
             rxm[f] = pm[o];
             rxp[f] = pp[o];
             if constexpr (EDGE) {
-                const double* pl = rb[f] + c * a.npts + i * plane;
-                rym[f] = gy_m ? __ldg(pl + wrap_idx(-1, n, a.g.bc) * n + kx) : bx[-TBW3];
-                ryp[f] = gy_p ? __ldg(pl + wrap_idx(n, n, a.g.bc) * n + kx) : bx[TBW3];
-                rzm[f] = gz_m ? __ldg(pl + (long)jy * n + wrap_idx(-1, n, a.g.bc)) : bx[-1];
-                rzp[f] = gz_p ? __ldg(pl + (long)jy * n + wrap_idx(n, n, a.g.bc)) : bx[1];
+                // ghost rows / columns from the side slots the copy engine filled
+                const double* sd = pc + SIDE + (f * NC + c) * side3(IY);
+                rym[f] = gy_m ? sd[2 + lx] : bx[-TBW3];
+                ryp[f] = gy_p ? sd[GROW3 + 2 + lx] : bx[TBW3];
+                rzm[f] = gz_m ? sd[2 * GROW3 + (1 + ly) * 2 + (int)(wrap_idx(-1, n, a.g.bc) & 1)]
+                              : bx[-1];
+                rzp[f] = gz_p ? sd[2 * GROW3 + gcol3(IY) + (1 + ly) * 2 +
+                                   (int)(wrap_idx(n, n, a.g.bc) & 1)]
+                              : bx[1];
             } else {
                 rym[f] = bx[-TBW3];
                 ryp[f] = bx[TBW3];
@@ -213,7 +242,7 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
 
 
 template <class P, int EV, int EP, int K, int S>
-__global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
     static_assert(S >= 4, "plane ring needs i-1, i, i+1 and one in flight");
     constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
     constexpr int NR = nraw<EV>();
@@ -231,9 +260,6 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
     const long nitems = (long)((n + I3X - 1) / I3X) * ((n + IY - 1) / IY) *
                         ((rows + SEG3 - 1) / SEG3);
     const long G = gridDim.x;
-    const double* rb[2];
-    const double* rh[2];
-    raw_fields<EV>(a, rb, rh);
 
     // Issue the plane S sequence numbers after position `pos` of item t
     // (if any) into stage s.
@@ -301,7 +327,11 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
     int q0 = 0;  // sequence number of position 0 of the current item
     for (long t = blockIdx.x; t < nitems; t += G) {
         const Item3 it = item3<IY>(t, n, rows);
+#ifdef EK_NOEDGE3  // timing experiment only: wrong results on boundary items
+        const bool edge = false;
+#else
         const bool edge = it.k0 < 1 || it.k0 + I3X >= n || it.j0 < 1 || it.j0 + IY >= n;
+#endif
         wait_full(q0);
         wait_full(q0 + 1);
         int sm = q0 % S, sc = (q0 + 1) % S;
@@ -320,7 +350,6 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
             const double* pm = smem + sm * SD;
             const double* pc = smem + sc * SD;
             const double* pp = smem + sp * SD;
-            const long i = it.i0 + p - 1;
 #pragma unroll
             for (int r = 0; r < PPT; ++r) {
                 int ly, lx;
@@ -328,11 +357,11 @@ __global__ void __launch_bounds__(T3, 2) k_tma3d(const KArgs a, const __grid_con
                 const int jy = it.j0 + ly, kx = it.k0 + lx;
                 const int ro = (1 + ly) * TBW3 + 2 + lx, co = ly * I3X + lx;
                 if (!edge)
-                    tma3_point<P, EV, EP, K, IY, false>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co,
-                                                        n, off[r], acc);
+                    tma3_point<P, EV, EP, K, IY, false>(a, ctl, pm, pc, pp, ly, lx, jy, kx, ro,
+                                                        co, n, off[r], acc);
                 else if (jy < n && kx < n)
-                    tma3_point<P, EV, EP, K, IY, true>(a, ctl, pm, pc, pp, rb, i, jy, kx, ro, co,
-                                                       n, off[r], acc);
+                    tma3_point<P, EV, EP, K, IY, true>(a, ctl, pm, pc, pp, ly, lx, jy, kx, ro,
+                                                       co, n, off[r], acc);
                 off[r] += plane;
             }
             release(q0 + p - 1, t, it, p - 1);
