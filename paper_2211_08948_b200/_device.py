@@ -20,6 +20,14 @@ F64 = torch.float64
 # ---------------------------------------------------------------- device
 
 _READY = False
+_DEVICES = {}
+# current device index without torch.cuda.current_device()'s lazy-init checks
+# (the host path asks ~100 times per integrator step); valid once _READY
+_GET_DEVICE = getattr(torch._C, "_cuda_getDevice", None)
+
+
+def _index():
+    return _GET_DEVICE() if _GET_DEVICE is not None else torch.cuda.current_device()
 
 
 def device():
@@ -29,8 +37,13 @@ def device():
             raise RuntimeError("paper_2211_08948_b200 needs a CUDA device (B200); "
                                "there is no CPU fallback")
         N.lib()
+        torch.cuda.init()
         _READY = True
-    return torch.device("cuda", torch.cuda.current_device())
+    i = _index()
+    d = _DEVICES.get(i)
+    if d is None:
+        d = _DEVICES[i] = torch.device("cuda", i)
+    return d
 
 
 _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
@@ -39,6 +52,8 @@ _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 def stream():
     """torch's current stream on the current device (raw handle; the fast
     accessor avoids building a torch.cuda.Stream object per call)."""
+    if _RAW_STREAM is not None and _READY:
+        return C.c_void_p(_RAW_STREAM(_index()))
     if _RAW_STREAM is not None:
         return C.c_void_p(_RAW_STREAM(torch.cuda.current_device()))
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -98,7 +113,7 @@ _WORK = {}
 
 def work(nbytes=None):
     """Per-device scratch for block partials (grows monotonically)."""
-    dev = torch.cuda.current_device()
+    dev = device().index
     need = max(int(nbytes or 0), 148 * 16 * 8 * 8)
     buf = _WORK.get(dev)
     if buf is None or buf.numel() * 8 < need:

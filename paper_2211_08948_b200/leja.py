@@ -163,12 +163,11 @@ class _CoefTable:
     def load(self, base, hi, dds, c, gamma, xi):
         h = self.host
         h[:] = 0.0
-        for m in range(base, hi):
-            col = m - base
-            if m >= 1:
-                h[col] = c / gamma + xi[m - 1]
-            for i, d in enumerate(dds):
-                h[(1 + i) * _CHUNK + col] = d[m]
+        lo = max(base, 1)
+        if hi > lo:  # c/gamma + xi[m-1]: one Python-float quotient, then fp64 adds
+            h[lo - base:hi - base] = (c / gamma) + np.asarray(xi[lo - 1:hi - 1], dtype=np.float64)
+        for i, d in enumerate(dds):
+            h[(1 + i) * _CHUNK:(1 + i) * _CHUNK + (hi - base)] = d[base:hi]
         N.check(N.lib().ek_copy(C.c_void_p(self.dev.data_ptr()),
                                 h.ctypes.data_as(C.c_void_p), h.nbytes, 1, D.stream()),
                 "coef upload")
