@@ -437,7 +437,7 @@ def run_reference(args, rank, world):
     return {"impl": "reference", "metric": METRIC, "value": val, "unit": "Jv/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": el / max(jvs, 1) * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded smooth perturbation of the Brusselator steady state",
             "config": config_dict(n, dt, {"step": "one FD Leja iteration (bounded sample)"}),
             "cpu_baseline": {"value": val, "unit": "Jv/s", "cores": 1, "kind": "port",

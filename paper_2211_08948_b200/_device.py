@@ -189,10 +189,19 @@ def norm2(x, st=None):
 
 
 def l1(x):
+    return l1_many([x])[0]
+
+
+def l1_many(xs):
+    """L1 norms of up to 8 device vectors: one reduction kernel each into
+    the slots of one state block, one host synchronisation."""
     st = scalar_state()
-    N.check(N.lib().ek_l1(x.numel(), C.c_void_p(x.data_ptr()), st.ptr, 0,
-                          work_ptr(), stream()), "ek_l1")
-    return global_sum(float(st.read().val[0]))
+    wp = work_ptr()
+    for i, x in enumerate(xs):
+        N.check(N.lib().ek_l1(x.numel(), C.c_void_p(x.data_ptr()), st.ptr, i,
+                              wp, stream()), "ek_l1")
+    h = st.read()
+    return [global_sum(float(h.val[i])) for i in range(len(xs))]
 
 
 # ------------------------------------------------------- vexpr builder
