@@ -200,3 +200,79 @@ def test_two_ranks_match_single_gpu(dim, n):
     # both ranks hold the same gathered results
     for x, y in zip(res[0]["vecs"], res[1]["vecs"]):
         assert np.array_equal(x, y)
+
+
+def _gpu_kiops_run(n, comm=None, dim=2):
+    """KIOPS on the full grid (fused Arnoldi passes) or this rank's slab
+    (`kiops._SlabArnoldi`: local device passes + rank-ordered global dots
+    and norms): kiops_eval of phi_1 and one EXPRB43 KIOPS step."""
+    import paper_2211_08948_b200 as ek
+    from paper_2211_08948_b200 import ext
+    prob = ext.brusselator_periodic_problem(n=n) if dim == 2 else ext.advdiff3d_problem(n=n)
+    if comm is not None:
+        prob = S.distribute(prob, comm)
+    rhs = ek.CountingRhs(prob.rhs)
+    sys_ = ek.make_linearized(rhs, prob.u0, jac_factory=prob.jac_factory)
+    lam, _ = ek.power_iterate(sys_.J)
+    dt = 30.0 / abs(lam)
+    f = np.asarray(sys_.f_n)
+    w, ks = ek.kiops_eval(sys_.J, [np.zeros_like(f), f * dt], dt, 1e-9)
+    st = ek.take_step("exprb43", sys_, dt, "kiops", 1e-8, ek.EngineContext())
+    vecs = [np.asarray(w), np.asarray(st.u_high)]
+    if comm is not None:
+        g = prob.rhs.global_grid
+        vecs = [comm.gather(v, g) for v in vecs]
+    return {"counts": (ks.matvecs, ks.substeps, ks.rejections, st.stats.krylov_matvecs,
+                       st.stats.substeps, rhs.counter.count),
+            "vecs": vecs}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,n", [(2, 96), (3, 34)])
+def test_kiops_slab_p1_matches_fused(dim, n):
+    """The slab KIOPS path at P = 1 against the fused
+    whole-grid Arnoldi: identical counts, vectors within the FD tier."""
+    from paper_2211_08948_b200 import _device as D
+    a = _gpu_kiops_run(n, dim=dim)
+    try:
+        b = _gpu_kiops_run(n, comm=S.SlabComm(), dim=dim)
+    finally:
+        D.COMM = None
+    assert a["counts"] == b["counts"]
+    for x, y in zip(a["vecs"], b["vecs"]):
+        assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y)
+
+
+def _gpu_kiops_worker(rank, world, port, n, q, dim):
+    _init(rank, world, port)
+    try:
+        torch.cuda.set_device(0)
+        q.put((rank, _gpu_kiops_run(n, comm=S.SlabComm(), dim=dim)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,n", [(2, 128), (3, 34)])
+def test_kiops_two_ranks_match_single_gpu(dim, n):
+    """Two slab ranks (host-staged gloo sums and halos, one GPU) take the
+    single-GPU run's KIOPS decisions: same matvecs / substeps / rejections,
+    vectors within the FD tier, identical on both ranks."""
+    ref = _gpu_kiops_run(n, dim=dim)
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_kiops_worker, args=(r, world, port, n, q, dim))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert res[r]["counts"] == ref["counts"]
+        for x, y in zip(res[r]["vecs"], ref["vecs"]):
+            assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y)
+    for x, y in zip(res[0]["vecs"], res[1]["vecs"]):
+        assert np.array_equal(x, y)
