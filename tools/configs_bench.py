@@ -162,6 +162,26 @@ def main():
                   "steps": steps, "ms_per_step_gpu": t / steps * 1e3,
                   "note": "includes the first step's power iteration (maybe_refresh)"})
 
+        # window (ii) of SURVEY.md §8(d) d8b: 20 adaptive steps from the
+        # reference's dt_init = 1e-5 t_final (t_final = 1), tol 1e-8
+        for scheme in ("leja", "kiops"):
+            run = lambda: ek.adaptive_loop(p.rhs, u0, 1.0, "epirk5p1", scheme, 1e-8,
+                                           ctx=ek.EngineContext(xi=xi), max_steps=20)
+            run()
+            sync()
+            t0 = time.perf_counter()
+            tr = run()
+            sync()
+            t = time.perf_counter() - t0
+            nst = tr.steps_accepted + tr.steps_rejected
+            emit({"config": 4, "problem": "brusselator_periodic 4096^2 x 2",
+                  "integrator": "epirk5p1", "scheme": scheme, "window": "adaptive",
+                  "steps": nst, "accepted": tr.steps_accepted, "t_reached": tr.t,
+                  "rhs_evals": tr.rhs_evals, "leja_iters": tr.leja_iters,
+                  "krylov_matvecs": tr.krylov_matvecs, "ms_per_step_gpu": t / max(1, nst) * 1e3,
+                  "note": "adaptive from dt_init = 1e-5 (tiny first steps: few Leja iterations "
+                          "each); includes the spectrum estimate"})
+
     # ---- config 5: adv-diff 512^3, EXPRB32 Leja, fixed dt = 50 dt_CFL
     if not only or "c5" in only:
         p = ext.advdiff3d_problem(n=512)
@@ -182,6 +202,24 @@ def main():
               "scheme": "leja", "dt_cfl_mult": 50.0, "steps": steps,
               "ms_per_step_gpu": t / steps * 1e3,
               "note": "includes the first step's power iteration (maybe_refresh)"})
+        # window (ii): 20 adaptive steps from dt_init = 1e-5 t_final, tol 1e-10
+        run = lambda: ek.adaptive_loop(p.rhs, u0, 1.0, "exprb32", "leja", 1e-10,
+                                       jac_factory=p.jac_factory,
+                                       ctx=ek.EngineContext(xi=xi), max_steps=20,
+                                       stepper=ext.take_step_ext,
+                                       order=ext.EXT_ORDER["exprb32"])
+        run()
+        sync()
+        t0 = time.perf_counter()
+        tr = run()
+        sync()
+        t = time.perf_counter() - t0
+        nst = tr.steps_accepted + tr.steps_rejected
+        emit({"config": 5, "problem": "advdiff3d 512^3", "integrator": "exprb32",
+              "scheme": "leja", "window": "adaptive", "steps": nst,
+              "accepted": tr.steps_accepted, "t_reached": tr.t, "leja_iters": tr.leja_iters,
+              "ms_per_step_gpu": t / max(1, nst) * 1e3,
+              "note": "adaptive from dt_init = 1e-5; includes the spectrum estimate"})
 
 
 if __name__ == "__main__":
