@@ -25,10 +25,12 @@ from pathlib import Path
 import numpy as np
 import torch
 
+from . import _ddpool
 from . import _device as D
 from . import _native as N
 from .errors import NonConvergence
-from .linalg import MatrixFreeOperator, dense_phi_action, fused_target
+from ._dense import phi_divided_differences
+from .linalg import MatrixFreeOperator, fused_target
 from .spectrum import SpectrumEstimate
 
 DEFAULT_NUM_POINTS = 400
@@ -100,19 +102,77 @@ _DD_CACHE = {}
 _DD_CACHE_MAX = 128
 
 
+def _dd_key(l, h, est, xi, m_max):
+    return (l, h, est.c, est.gamma, min(m_max, len(xi)), id(xi), len(xi),
+            float(xi[0]), float(xi[-1]))
+
+
+def _dd_store(key, d):
+    if len(_DD_CACHE) >= _DD_CACHE_MAX:
+        _DD_CACHE.pop(next(iter(_DD_CACHE)))
+    _DD_CACHE[key] = d
+
+
+def _dd_prefetch(l, h, est, xi, m_max):
+    """Start computing a later chunk's table in the worker pool (`_ddpool`):
+    tables beyond the first chunk (m > 32) are always computed there, one
+    BLAS thread each, so the bits do not depend on the caller's BLAS
+    threading and the host work runs beside the device work."""
+    m = min(m_max, len(xi))
+    if m <= _CHUNK or not 0 <= l <= 4 or h < 0:
+        return
+    key = _dd_key(l, h, est, xi, m)
+    if key in _DD_CACHE:
+        return
+    pool = _ddpool.existing()
+    if pool is not None:
+        try:
+            pool.submit(key, (l, h, est.c, est.gamma, np.asarray(xi, dtype=np.float64), m))
+        except Exception:  # noqa: BLE001 - worker trouble: compute in-process
+            _ddpool.disable()
+
+
 def _dd_cached(l, h, est, xi, m_max):
     """divided_differences(...).d memoised on its exact inputs: fixed-dt
     stepping and the 50-step spectrum reuse hit the same tables every step,
-    so the host expm (0.2-2.7 ms per table) is paid once."""
-    key = (l, h, est.c, est.gamma, min(m_max, len(xi)), id(xi), len(xi),
-           float(xi[0]), float(xi[-1]))
+    so the host expm (0.2-2.7 ms per table) is paid once. Tables beyond the
+    first chunk come from the worker pool (submitted ahead by the Leja loop
+    when it can)."""
+    key = _dd_key(l, h, est, xi, m_max)
     d = _DD_CACHE.get(key)
-    if d is None:
+    if d is not None:
+        return d
+    _dd_prefetch(l, h, est, xi, m_max)
+    pool = _ddpool.existing()
+    if pool is not None and pool.pending(key):
+        try:
+            ok, val = pool.collect(key)
+        except Exception:  # noqa: BLE001 - worker trouble: compute in-process
+            _ddpool.disable()
+            ok, val = False, None
+        if ok:
+            if not np.isfinite(val).all():  # as divided_differences()
+                raise NonConvergence("non-finite divided differences; spectral estimate invalid")
+            _dd_store(key, val)
+            return val
+    if min(m_max, len(xi)) > _CHUNK:
+        with _one_blas_thread():
+            d = divided_differences(l, h, est, xi, m_max).d
+        _ddpool.pool()  # a chunk crossing: have the workers ready for the next ones
+    else:
         d = divided_differences(l, h, est, xi, m_max).d
-        if len(_DD_CACHE) >= _DD_CACHE_MAX:
-            _DD_CACHE.pop(next(iter(_DD_CACHE)))
-        _DD_CACHE[key] = d
+    _dd_store(key, d)
     return d
+
+
+def _one_blas_thread():
+    """In-process fallback for large tables: the pool's one-thread BLAS."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=1, user_api="blas")
+    except ImportError:
+        import contextlib
+        return contextlib.nullcontext()
 
 
 def divided_differences(l, h, est: SpectrumEstimate, xi, m_max):
@@ -124,12 +184,7 @@ def divided_differences(l, h, est: SpectrumEstimate, xi, m_max):
     if h < 0:
         raise ValueError("scale h must be >= 0")
     m_max = min(m_max, len(xi))
-    L = np.diag(h * (est.c + est.gamma * xi[:m_max]))
-    r = np.arange(m_max - 1)
-    L[r + 1, r] = h * est.gamma
-    e1 = np.zeros(m_max)
-    e1[0] = 1.0
-    d = dense_phi_action(l, L, e1)
+    d = phi_divided_differences(l, h, est.c, est.gamma, xi, m_max)
     if not np.isfinite(d).all():
         raise NonConvergence("non-finite divided differences; spectral estimate invalid")
     return DividedDifferences(d=d, l=l, h=h, c=est.c, gamma=est.gamma)
@@ -226,6 +281,12 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
         raise ValueError(f"expected vector of length {J.dim}, got {n}")
 
     m_avail = min(_CHUNK, max_points)
+    # a group that needed more than one chunk last time (the engines pass its
+    # previous count + 1 as _first_batch) gets its later tables started now
+    ahead = min(max_points, (int(_first_batch) + _CHUNK // 2) // _CHUNK * _CHUNK + _CHUNK)
+    for mm in range(2 * _CHUNK, ahead + 1, _CHUNK):
+        for ci in coeffs:
+            _dd_prefetch(l, ci * h, est, xi, mm)
     dds = [_dd_cached(l, ci * h, est, xi, m_avail) for ci in coeffs]
     table = _CoefTable(k)
     table.load(0, min(_CHUNK, m_avail), dds, c, gamma, xi)
@@ -281,6 +342,8 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     while m < max_points:
         if m >= m_avail:  # next 32-point chunk (leja.py:168-171)
             m_avail = min(m_avail + _CHUNK, max_points)
+            for ci in coeffs:  # keep the pool one chunk ahead
+                _dd_prefetch(l, ci * h, est, xi, min(m_avail + _CHUNK, max_points))
             dds = [_dd_cached(l, ci * h, est, xi, m_avail) for ci in coeffs]
             base = m
             table.load(base, m_avail, dds, c, gamma, xi)
@@ -323,6 +386,11 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             if prof is not None:
                 ev[1].record()
                 prof["events"].append(ev)
+            if hi == m_avail < max_points:
+                # the next chunk's tables start in the
+                # worker pool while this batch runs on the device
+                for ci in coeffs:
+                    _dd_prefetch(l, ci * h, est, xi, min(m_avail + _CHUNK, max_points))
             hst = st.read()
             if prof is not None:
                 prof["iters"] = int(hst.m)

@@ -338,63 +338,5 @@ def fd_jacobian_apply(f, u, v, fu=None):
 
 
 # ------------------------------------------------------- small dense (host)
-
-def dense_expm(M):
-    """exp(M) of a small dense matrix by scipy's Pade scaling-and-squaring
-    (linalg.py:132-139) — the same function the reference calls."""
-    M = np.asarray(M, dtype=float)
-    if M.ndim != 2 or M.shape[0] != M.shape[1]:
-        raise ValueError("dense_expm expects a square matrix")
-    if not np.isfinite(M).all():
-        raise FloatingPointError("non-finite entries in dense_expm input")
-    return scipy.linalg.expm(M)
-
-
-def _phi_taylor(l, M, terms=20):
-    """sum_k M^k / (k+l)!  for tiny ||M|| (linalg.py:142-150)."""
-    acc = np.zeros_like(M)
-    power = np.eye(M.shape[0])
-    for k in range(terms):
-        acc += power / math.factorial(k + l)
-        power = power @ M
-    return acc
-
-
-def dense_phi(l, M):
-    """phi_l(M) via the block upper-bidiagonal embedding (linalg.py:153-175)."""
-    M = np.asarray(M, dtype=float)
-    if M.ndim != 2 or M.shape[0] != M.shape[1]:
-        raise ValueError("dense_phi expects a square matrix")
-    if l < 0:
-        raise ValueError("phi order must be >= 0")
-    if l == 0:
-        return dense_expm(M)
-    if np.linalg.norm(M) < 1e-8:
-        return _phi_taylor(l, M)
-    n = M.shape[0]
-    big = np.zeros(((l + 1) * n, (l + 1) * n))
-    big[:n, :n] = M
-    eye = np.eye(n)
-    for k in range(l):
-        big[k * n:(k + 1) * n, (k + 1) * n:(k + 2) * n] = eye
-    return dense_expm(big)[:n, -n:]
-
-
-def dense_phi_action(l, M, b):
-    """phi_l(M) b from one (n+l)-dimensional exponential (linalg.py:178-199)."""
-    M = np.asarray(M, dtype=float)
-    n = M.shape[0]
-    if b.shape != (n,):
-        raise ValueError("vector length mismatch in dense_phi_action")
-    if l == 0:
-        return dense_expm(M) @ b
-    if np.linalg.norm(M) < 1e-8:
-        return _phi_taylor(l, M) @ b
-    aug = np.zeros((n + l, n + l))
-    aug[:n, :n] = M
-    aug[:n, n] = b
-    idx = np.arange(l - 1)
-    aug[n + idx, n + idx + 1] = 1.0
-    last = np.zeros(n + l)
-    last[-1] = 1.0
-    return (dense_expm(aug) @ last)[:n]
+# torch-free module: the divided-difference worker processes run the same code
+from ._dense import _phi_taylor, dense_expm, dense_phi, dense_phi_action  # noqa: E402,F401
