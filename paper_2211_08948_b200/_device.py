@@ -149,12 +149,44 @@ class DevState:
         N.check(N.lib().ek_copy(self.ptr, C.byref(self.host), self.size, 1, stream()),
                 "state upload")
 
-    def read(self):
-        """Stream-ordered D2H copy into pageable memory: returns once the
-        stream has reached this point (the host sync of a chunk)."""
+    def _pull(self):
         N.check(N.lib().ek_copy(C.byref(self.host), self.ptr, self.size, 2, stream()),
                 "state read")
         return self.host
+
+    def read(self):
+        """Stream-ordered D2H copy into pageable memory: returns once the
+        stream has reached this point (the host sync of a chunk). Deferred
+        checks of earlier passes are resolved first (program order)."""
+        self._pull()
+        if _PENDING:
+            flush_checks()
+        return self.host
+
+
+# Deferred error checks (single GPU): a pass whose state carries only an
+# error flag (the remainder's non-finite test, integrators.py:107-108) is
+# not synchronised on by itself; its flag is checked at the stream's next
+# host sync, before that sync's own result is interpreted (so the
+# reference's exception, and no later work's counter charges, wins), and at
+# the end of the step. The host keeps enqueueing while the pass runs.
+_PENDING = []
+
+
+def defer_check(state, mask, make_exc):
+    _PENDING.append((state, mask, make_exc))
+
+
+def clear_checks():
+    _PENDING.clear()
+
+
+def flush_checks():
+    while _PENDING:
+        st, mask, make_exc = _PENDING.pop(0)
+        if st._pull().flag & mask:
+            _PENDING.clear()
+            raise make_exc()
 
 
 def scalar_state():

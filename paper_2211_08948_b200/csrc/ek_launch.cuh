@@ -108,9 +108,10 @@ constexpr int tma_stages2() {
 template <int EV, int EP, int NC, int K>
 constexpr int tma_stages3() {
     constexpr int bytes = stage3_doubles<EV, EP, NC, K>() * 8;
-    constexpr int two = (110 * 1024) / bytes, one = (220 * 1024) / bytes;
+    // per-block budget: 220 KB of shared memory over EK_LB3 resident blocks
+    constexpr int two = (220 * 1024 / EK_LB3) / bytes, one = (220 * 1024) / bytes;
 #ifdef EK_S3
-    if (EK_S3 > 0 && EK_S3 * bytes <= (EK_LB3 == 1 ? 220 : 110) * 1024) return EK_S3;
+    if (EK_S3 > 0 && EK_S3 * bytes <= 220 * 1024 / EK_LB3) return EK_S3;
 #endif
     if (EK_LB3 == 1) return one >= 5 ? (one > 16 ? 16 : one) : 0;
     // 5 stages (i-1, i, i+1 resident, two planes in flight) measured best on

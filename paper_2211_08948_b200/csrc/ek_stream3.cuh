@@ -82,7 +82,7 @@ __host__ __device__ constexpr int iy3() {
 #ifdef EK_IY3
     if (EK_IY3 == 8 || stage3_doubles_iy<EV, EP, NC, K>(16) * 8 * 5 <= 220 * 1024) return EK_IY3;
 #endif
-    return (110 * 1024) / (stage3_doubles_iy<EV, EP, NC, K>(16) * 8) >= 5 ? 16 : 8;
+    return (220 * 1024 / EK_LB3) / (stage3_doubles_iy<EV, EP, NC, K>(16) * 8) >= 5 ? 16 : 8;
 }
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage3_doubles() {
