@@ -215,6 +215,18 @@ int ek_remainder_combo(const ek_grid* g, int jac, const double* u, const double*
                        const double* xin, const double* xa, const double* xr,
                        const double* xf, ek_scalar_state* st, double* work,
                        const double* const* halo, void* stream);
+/* ek_remainder_combo with the direction test on the device: pre is the
+ * state of the pass that formed k (val[1] = ||k - u_n||, flag bit0 =
+ * k != u_n), nu points at ||u_n|| (FD only). The FD increment
+ * eps = (sqrt(EPS) * (1 + ||u_n||)) / ||k - u_n|| (linalg.py:123) is formed by
+ * the kernel in Python's order; if k == u_n the outputs take R = 0
+ * (integrators.py:104-105). No host round trip between the two passes. */
+int ek_remainder_combo_dev(const ek_grid* g, int jac, const double* u, const double* fu,
+                           const double* k, const ek_scalar_state* pre, const double* nu,
+                           double* out, int nx, double* const* xo, const double* xin,
+                           const double* xa, const double* xr, const double* xf,
+                           ek_scalar_state* st, double* work, const double* const* halo,
+                           void* stream);
 
 /* ------------------------------------------------------- Leja (leja.py) */
 /* Coefficient table coef_dev: (k+1) rows x 32 columns, row 0 the shifts

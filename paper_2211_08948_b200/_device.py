@@ -170,11 +170,20 @@ class DevState:
 # host sync, before that sync's own result is interpreted (so the
 # reference's exception, and no later work's counter charges, wins), and at
 # the end of the step. The host keeps enqueueing while the pass runs.
+# Deferred counter charges (defer_fn callbacks) add what they charge to
+# ADJ[0], so that per-group counter windows opened before a flush can leave
+# them out (integrators._Engines._charge).
 _PENDING = []
+ADJ = [0]
 
 
 def defer_check(state, mask, make_exc):
     _PENDING.append((state, mask, make_exc))
+
+
+def defer_fn(state, fn):
+    """fn(host_state) at the next flush (in program order with the checks)."""
+    _PENDING.append((state, None, fn))
 
 
 def clear_checks():
@@ -183,10 +192,13 @@ def clear_checks():
 
 def flush_checks():
     while _PENDING:
-        st, mask, make_exc = _PENDING.pop(0)
-        if st._pull().flag & mask:
+        st, mask, fn = _PENDING.pop(0)
+        h = st._pull()
+        if mask is None:
+            fn(h)
+        elif h.flag & mask:
             _PENDING.clear()
-            raise make_exc()
+            raise fn()
 
 
 def scalar_state():
@@ -433,12 +445,14 @@ def _lincomb(outputs, length, rmode):
     return ins, nterm, src, mode, coef, coef2, fin, fval
 
 
-def evaluate(outputs, length, norm=False, check=False, norm_diff=False):
+def evaluate(outputs, length, norm=False, check=False, norm_diff=False, lazy=False):
     """Run one fused elementwise pass.
 
     outputs: list of (Expr, out_tensor_or_None). norm/check apply to the
     first expression (norm_diff: to the difference of the first two):
     returns (||value||, flags) after a sync when requested, else None.
+    lazy (single GPU): return the unread state block of the reducing pass
+    instead (linear combinations only; other expressions sync as usual).
     Linear combinations go to `ek_lincomb`; anything else to the general
     elementwise program `ek_vexpr`."""
     rmode = 2 if norm_diff else (1 if (norm or check) else 0)
@@ -453,6 +467,8 @@ def evaluate(outputs, length, norm=False, check=False, norm_diff=False):
             stream()), "ek_lincomb")
         if st is None:
             return None
+        if lazy and COMM is None:
+            return st
         return global_norm(st.read())
     if norm_diff:
         a, b = outputs[0][0], outputs[1][0]

@@ -97,6 +97,9 @@ _SIGS = {
     "ek_remainder": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _P, _P, _PP, _P]),
     "ek_remainder_combo": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _D, _P, _I, _PP, _P,
                                 C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), _P, _P, _PP, _P]),
+    "ek_remainder_combo_dev": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _P, _P, _P, _I, _PP, _P,
+                                    C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), _P, _P, _PP,
+                                    _P]),
     "ek_leja_begin_len": (_I, [_L, _P, _PP, _I, _P, _P, _P, _P]),
     "ek_leja_run": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
                          _I, _I, _D, _P, _P, _PP, _P]),

@@ -240,6 +240,10 @@ struct KArgs {
     const double* xin;
     double xa[3], xr[3], xf[3];
     int nxo;
+    // EP_REM with the direction norm on the device (ek_remainder_combo_dev):
+    // pre->val[1] = ||k - u_n||, pre->flag bit0 = k != u_n; *nu = ||u_n||
+    const ek_scalar_state* pre;
+    const double* nu;
 };
 
 // ----------------------------------------------------------------- geometry
@@ -445,7 +449,15 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
                            ? a.win[a.nwin - 1][n + a.aug_tail[t]] * a.aug_scale : 0.0;
         }
     }
-    if constexpr (EP == EP_REM) ctl.active = a.xin ? 1u : 0u;  // centre slot 0 = xin
+    if constexpr (EP == EP_REM) {
+        ctl.active = a.xin ? 1u : 0u;  // centre slot 0 = xin
+        if (a.pre) {
+            // `if not np.any(dk)`: R = 0 (integrators.py:104-105)
+            ctl.y_zero = (a.pre->flag & 1) == 0;
+            // eps = sqrt(EPS) * (1 + ||u||) / ||dk||, Python's order (linalg.py:123)
+            if (EV == EV_REMFD) ctl.eps = (SQRT_EPS * (1.0 + *a.nu)) / a.pre->val[1];
+        }
+    }
     ctl.h_first = ctl.h_second = ctl.h_penult = ctl.h_last = nullptr;
     ctl.rowlen = 0;
     if constexpr (EP == EP_LEJA) {
@@ -588,19 +600,20 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
                 if (q < a.nwin) acc[q] += z.p[q][c] * w;
             if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
         } else {  // EP_REM
-            if (a.out) st_stream(a.out + e, v, ctl.wpol);
+            const double r = ctl.y_zero ? 0.0 : v;  // zero direction (device-side test)
+            if (a.out) st_stream(a.out + e, r, ctl.wpol);
             if (a.nxo) {  // the stage algebra that consumes R, in registers
                 const double xin = K > 0 ? z.p[0][c] : 0.0;  // staged with the pass
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     if (q < a.nxo) {
-                        const double rv = a.xr[q] * v;
+                        const double rv = a.xr[q] * r;
                         const double t = K > 0 ? (a.xa[q] * xin) + rv : rv;
                         st_stream(a.xo[q] + e, t * a.xf[q], ctl.wpol);
                     }
                 }
             }
-            acc[0] += isfinite(v) ? 0.0 : 1.0;
+            acc[0] += isfinite(r) ? 0.0 : 1.0;
         }
     }
 }

@@ -323,12 +323,17 @@ int ek_remainder(const ek_grid* g, int jac, const double* u, const double* fu, c
     return launch_stencil<EP_REM>(ev, a, (cudaStream_t)stream);
 }
 
-int ek_remainder_combo(const ek_grid* g, int jac, const double* u, const double* fu,
-                       const double* k, double eps, double* out, int nx, double* const* xo,
-                       const double* xin, const double* xa, const double* xr, const double* xf,
-                       ek_scalar_state* st, double* work, const double* const* halo,
-                       void* stream) {
+static int remainder_combo(const ek_grid* g, int jac, const double* u, const double* fu,
+                           const double* k, double eps, const ek_scalar_state* pre,
+                           const double* nu, double* out, int nx, double* const* xo,
+                           const double* xin, const double* xa, const double* xr,
+                           const double* xf, ek_scalar_state* st, double* work,
+                           const double* const* halo, void* stream) {
     if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (pre && jac == EK_JAC_FD && !nu) {
+        set_error("ek_remainder_combo_dev: FD needs the device ||u_n||");
+        return EK_ERR_INVALID;
+    }
     if (nx < 0 || nx > 3 || (nx > 0 && (!xo || !xr || !xf || (xin && !xa))) || (!out && nx == 0)) {
         set_error("ek_remainder_combo: bad outputs (nx=%d)", nx);
         return EK_ERR_INVALID;
@@ -348,6 +353,7 @@ int ek_remainder_combo(const ek_grid* g, int jac, const double* u, const double*
     KArgs a;
     base_args(a, g, halo);
     a.u = u; a.fu = fu; a.k = k; a.eps = eps; a.out = out; a.st = st; a.work = work;
+    a.pre = pre; a.nu = nu;
     a.nxo = nx;
     a.xin = xin;
     for (int q = 0; q < nx; ++q) {
@@ -357,6 +363,29 @@ int ek_remainder_combo(const ek_grid* g, int jac, const double* u, const double*
         a.xf[q] = xf[q];
     }
     return launch_stencil<EP_REM>(ev, a, (cudaStream_t)stream);
+}
+
+int ek_remainder_combo(const ek_grid* g, int jac, const double* u, const double* fu,
+                       const double* k, double eps, double* out, int nx, double* const* xo,
+                       const double* xin, const double* xa, const double* xr, const double* xf,
+                       ek_scalar_state* st, double* work, const double* const* halo,
+                       void* stream) {
+    return remainder_combo(g, jac, u, fu, k, eps, nullptr, nullptr, out, nx, xo, xin, xa, xr,
+                           xf, st, work, halo, stream);
+}
+
+int ek_remainder_combo_dev(const ek_grid* g, int jac, const double* u, const double* fu,
+                           const double* k, const ek_scalar_state* pre, const double* nu,
+                           double* out, int nx, double* const* xo, const double* xin,
+                           const double* xa, const double* xr, const double* xf,
+                           ek_scalar_state* st, double* work, const double* const* halo,
+                           void* stream) {
+    if (!pre) {
+        set_error("ek_remainder_combo_dev: pre is required");
+        return EK_ERR_INVALID;
+    }
+    return remainder_combo(g, jac, u, fu, k, 0.0, pre, nu, out, nx, xo, xin, xa, xr, xf, st,
+                           work, halo, stream);
 }
 
 // ------------------------------------------------------------------- Leja

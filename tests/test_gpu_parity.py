@@ -302,3 +302,35 @@ def test_ext_problem_steps(golden, xi, name):
     assert rel(r2.u_high, g("exprb2")) <= tolv
     r3 = ext.take_step_ext("exprb32", sys_, dt, "leja", 1e-10, ctx)
     assert rel(r3.u_high, g("exprb32")) <= tolv
+
+
+@pytest.mark.parametrize("integ", ["epirk5p1", "exprb43"])
+@pytest.mark.parametrize("name,state", [("brusselator_periodic", (1.0, 3.0)),
+                                        ("allen_cahn_periodic", (1.0,))])
+def test_zero_direction_stage_remainders(xi, integ, name, state):
+    """Steps from an exact steady state (f(u_n) = 0): every stage equals u_n,
+    so each fused remainder takes the k == u_n branch (R = 0, no RHS charge,
+    integrators.py:104-105) — decided on the device by
+    ek_remainder_combo_dev and charged at the next host sync. Counts, groups
+    and the result must match the oracle's step exactly."""
+    n = 16
+    p = getattr(ext, f"{name}_problem")(n=n)
+    q = getattr(OF, name)(n=n)
+    u = np.concatenate([np.full(n * n, v) for v in state])
+    rhs = ek.CountingRhs(p.rhs)
+    sys_ = ek.make_linearized(rhs, u)
+    assert not np.any(sys_.f_n)
+    from oracle import np_phi as OP
+    orhs = OP.CountedRhs(q.rhs)
+    osys = OI.linearize(orhs, u)
+    lam, _ = ek.power_iterate(ek.make_linearized(ek.CountingRhs(p.rhs), p.u0).J)
+    est = ek.make_estimate(lam)
+    dt = 10.0 / abs(est.alpha)
+    c0, o0 = rhs.counter.count, orhs.counter.count
+    st = ek.take_step(integ, sys_, dt, "leja", 1e-8, ek.EngineContext(est=est, xi=xi))
+    ost = OI.step(integ, osys, dt, "leja", 1e-8, OI.Ctx(est=est, xi=xi))
+    assert rhs.counter.count - c0 == orhs.counter.count - o0
+    assert st.stats.leja_iters == ost.stats.leja_iters
+    assert dict(st.stats.group_rhs_evals) == dict(ost.stats.group_rhs_evals)
+    assert np.array_equal(st.u_high, ost.u_high)
+    assert st.err_est == ost.err_est
