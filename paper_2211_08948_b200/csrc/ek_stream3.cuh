@@ -167,17 +167,21 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
 
 // One point (i, jy, kx) from the stages of planes i-1 (pm), i (pc), i+1 (pp);
 // ro / co: its offset inside a raw / centre slot.
-template <class P, int EV, int EP, int K, int IY, bool EDGE>
+// EDGE: bit 0 = the item touches a y edge (j = 0 / n-1), bit 1 = a z edge
+// (k = 0 / n-1); only those ghost selects are compiled in. zpar: the
+// column parity of the wrapped ghost columns -1 / n (launch constants).
+template <class P, int EV, int EP, int K, int IY, int EDGE>
 __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                            const double* pc, const double* pp,
                                            int ly, int lx, int jy, int kx, int ro, int co, int n,
-                                           long off, double* acc) {
+                                           long off, double* acc, int zpm, int zpp) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     constexpr int RAW3 = raw3(IY), CTR3 = ctr3(IY);
     constexpr int SIDE = NR * NC * RAW3 + nctr_maps<EV, EP, K>() * NC * CTR3;
-    const bool gy_m = EDGE && jy == 0, gy_p = EDGE && jy == n - 1;
-    const bool gz_m = EDGE && kx == 0, gz_p = EDGE && kx == n - 1;
+    constexpr bool EY = (EDGE & 1) != 0, EZ = (EDGE & 2) != 0;
+    const bool gy_m = EY && jy == 0, gy_p = EY && jy == n - 1;
+    const bool gz_m = EZ && kx == 0, gz_p = EZ && kx == n - 1;
     Nb nb[NC][NCH];
     double yc[NC];
 #pragma unroll
@@ -190,19 +194,19 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
             rc[f] = bx[0];
             rxm[f] = pm[o];
             rxp[f] = pp[o];
-            if constexpr (EDGE) {
-                // ghost rows / columns from the side slots the copy engine filled
-                const double* sd = pc + SIDE + (f * NC + c) * side3(IY);
+            // ghost rows / columns from the side slots the copy engine filled
+            const double* sd = pc + SIDE + (f * NC + c) * side3(IY);
+            if constexpr (EY) {
                 rym[f] = gy_m ? sd[2 + lx] : bx[-TBW3];
                 ryp[f] = gy_p ? sd[GROW3 + 2 + lx] : bx[TBW3];
-                rzm[f] = gz_m ? sd[2 * GROW3 + (1 + ly) * 2 + (int)(wrap_idx(-1, n, a.g.bc) & 1)]
-                              : bx[-1];
-                rzp[f] = gz_p ? sd[2 * GROW3 + gcol3(IY) + (1 + ly) * 2 +
-                                   (int)(wrap_idx(n, n, a.g.bc) & 1)]
-                              : bx[1];
             } else {
                 rym[f] = bx[-TBW3];
                 ryp[f] = bx[TBW3];
+            }
+            if constexpr (EZ) {
+                rzm[f] = gz_m ? sd[2 * GROW3 + (1 + ly) * 2 + zpm] : bx[-1];
+                rzp[f] = gz_p ? sd[2 * GROW3 + gcol3(IY) + (1 + ly) * 2 + zpp] : bx[1];
+            } else {
                 rzm[f] = bx[-1];
                 rzp[f] = bx[1];
             }
@@ -324,13 +328,15 @@ __global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __gri
         }
     };
 
+    const int zpm = (int)(wrap_idx(-1, n, a.g.bc) & 1), zpp = (int)(wrap_idx(n, n, a.g.bc) & 1);
     int q0 = 0;  // sequence number of position 0 of the current item
     for (long t = blockIdx.x; t < nitems; t += G) {
         const Item3 it = item3<IY>(t, n, rows);
 #ifdef EK_NOEDGE3  // timing experiment only: wrong results on boundary items
-        const bool edge = false;
+        const int edge = 0;
 #else
-        const bool edge = it.k0 < 1 || it.k0 + I3X >= n || it.j0 < 1 || it.j0 + IY >= n;
+        const int edge = ((it.j0 < 1 || it.j0 + IY >= n) ? 1 : 0) |
+                         ((it.k0 < 1 || it.k0 + I3X >= n) ? 2 : 0);
 #endif
         wait_full(q0);
         wait_full(q0 + 1);
@@ -356,12 +362,22 @@ __global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __gri
                 point_of(r, ly, lx);
                 const int jy = it.j0 + ly, kx = it.k0 + lx;
                 const int ro = (1 + ly) * TBW3 + 2 + lx, co = ly * I3X + lx;
-                if (!edge)
-                    tma3_point<P, EV, EP, K, IY, false>(a, ctl, pm, pc, pp, ly, lx, jy, kx, ro,
-                                                        co, n, off[r], acc);
-                else if (jy < n && kx < n)
-                    tma3_point<P, EV, EP, K, IY, true>(a, ctl, pm, pc, pp, ly, lx, jy, kx, ro,
-                                                       co, n, off[r], acc);
+                if (edge == 0)
+                    tma3_point<P, EV, EP, K, IY, 0>(a, ctl, pm, pc, pp, ly, lx, jy, kx, ro,
+                                                    co, n, off[r], acc, zpm, zpp);
+                else if (jy < n && kx < n) {
+                    // y-edge items: only the rows j = 0 / n-1 need the selects
+                    const int e = edge & ~((jy > 0 && jy < n - 1) ? 1 : 0);
+                    if (e == 2)
+                        tma3_point<P, EV, EP, K, IY, 2>(a, ctl, pm, pc, pp, ly, lx, jy, kx,
+                                                        ro, co, n, off[r], acc, zpm, zpp);
+                    else if (e == 0)
+                        tma3_point<P, EV, EP, K, IY, 0>(a, ctl, pm, pc, pp, ly, lx, jy, kx,
+                                                        ro, co, n, off[r], acc, zpm, zpp);
+                    else
+                        tma3_point<P, EV, EP, K, IY, 3>(a, ctl, pm, pc, pp, ly, lx, jy, kx,
+                                                        ro, co, n, off[r], acc, zpm, zpp);
+                }
                 off[r] += plane;
             }
             release(q0 + p - 1, t, it, p - 1);
