@@ -179,16 +179,27 @@ struct PBurgers {
 };
 
 // BASELINE config 5. prm: D, vx, vy, vz. Linear.
-struct PAdvDiff3 {
+// FWD: instantiation for velocities >= 0 on every axis (the launcher picks
+// it from the parameters): the forward differences without the operand
+// selects (12 FSEL per point), the same subtraction and quotient.
+template <bool FWD>
+struct PAdvDiff3T {
     static constexpr int NC = 1, DIM = 3;
     static constexpr bool LINEAR = true;
     __device__ static void f(const Nb (&s)[1], double (&o)[1], const PC& g) {
         const Nb& q = s[0];
-        o[0] = (((g.prm[0] * lap3(q, g)) + (g.prm[1] * upw_x(q, g.prm[1], g)))
-                + (g.prm[2] * upw_y(q, g.prm[2], g)))
-               + (g.prm[3] * upw_z(q, g.prm[3], g));
+        if constexpr (FWD) {
+            o[0] = (((g.prm[0] * lap3(q, g)) + (g.prm[1] * dv(q.xp - q.c, g.h)))
+                    + (g.prm[2] * dv(q.yp - q.c, g.h)))
+                   + (g.prm[3] * dv(q.zp - q.c, g.h));
+        } else {
+            o[0] = (((g.prm[0] * lap3(q, g)) + (g.prm[1] * upw_x(q, g.prm[1], g)))
+                    + (g.prm[2] * upw_y(q, g.prm[2], g)))
+                   + (g.prm[3] * upw_z(q, g.prm[3], g));
+        }
     }
 };
+using PAdvDiff3 = PAdvDiff3T<false>;
 
 // ------------------------------------------------------------- launch args
 
