@@ -24,7 +24,7 @@ import numpy as np
 from . import _device as D
 from . import _native as N
 from .integrators import (INTEGRATOR_ORDER, StepResult, StepStats, _Engines,
-                          _check_scheme, take_step)
+                          _check_scheme, run_stepper, take_step)
 from .problems import NativeJacFactory, Problem, StencilRhs, make_grid
 
 X = D.V
@@ -199,7 +199,7 @@ def take_step_ext(name, sys, dt, scheme, tol, ctx):
     if name in EXT_STEPPERS:
         if dt <= 0:
             raise ValueError("dt must be positive")
-        return EXT_STEPPERS[name](sys, dt, scheme, tol, ctx)
+        return run_stepper(EXT_STEPPERS[name], sys, dt, scheme, tol, ctx)
     return take_step(name, sys, dt, scheme, tol, ctx)
 
 

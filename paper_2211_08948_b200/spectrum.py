@@ -69,6 +69,8 @@ _POWER_BATCH = 8
 def power_iterate(J: MatrixFreeOperator, tol_pi=1e-2, max_it=1000, seed=0):
     """Dominant |lambda| of J by power iteration (spectrum.py:43-63).
     Returns (estimate, converged)."""
+    if max_it <= 0:  # the reference's loop body never runs (spectrum.py:53-63)
+        return 0.0, False
     fused = fused_target(J)
     if fused is not None and fused[0].comm is not None:
         # slab mode: this rank's rows of the global seeded start vector
