@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--grid", type=int, default=N_GRID)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other BASELINE configs (the 'configs' key)")
+    ap.add_argument("--configs-budget", type=float, default=120.0)
     return ap.parse_args()
 
 
@@ -290,8 +293,12 @@ def run_ours(args, rank, world, local):
 
     if not args.no_e2e:
         out["e2e"] = e2e(args, ek, prob, dt, xi, world)
+    if world == 1 and not args.no_configs:
+        del prob, u
+        torch.cuda.empty_cache()
+        out["configs"] = secondary_configs(ek, xi, budget_s=args.configs_budget)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(n, dt)
+        out["cpu_baseline"] = cpu_baseline(n, lam)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -346,17 +353,175 @@ def e2e(args, ek, prob, dt, xi, world=1):
                    "StepResult.u_high (numpy)"}
 
 
+# ------------------------------------------------- the other BASELINE configs
+
+def secondary_configs(ek, xi, budget_s=120.0):
+    """The other BASELINE.json configs, each timed on the device after one
+    untimed run (wall clock around a synchronised run of the public API —
+    small grids are host-latency bound, so the host time is the number),
+    with the discrete counts. Config 5 also reports the fused 3-D Leja
+    kernel's roofline fraction (linear Jv: 8N(2+2k_active) per launch,
+    CUDA events). Skipped configs (budget) say so."""
+    import torch
+    from paper_2211_08948_b200 import ext
+    from paper_2211_08948_b200 import leja as L
+    t_start = time.perf_counter()
+    out = {}
+
+    def timed(run, reps=1):
+        run()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = run()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / reps, r
+
+    def left():
+        return budget_s - (time.perf_counter() - t_start)
+
+    # config 1: adv-diff 64^2, one EXPRB2 Leja step at dt = 50 dt_CFL, Pe 1 and 10
+    for pe in (1.0, 10.0):
+        p = ext.advdiff2d_problem(n=64, peclet=pe)
+        dt = 50.0 * p.params["dt_cfl"]
+        t, _ = timed(lambda: ek.fixed_step_loop(p.rhs, p.u0, dt, 1, "exprb2", "leja", 1e-10,
+                                                jac_factory=p.jac_factory,
+                                                ctx=ek.EngineContext(xi=xi),
+                                                stepper=ext.take_step_ext), reps=20)
+        out[f"config1_pe{pe:g}"] = {
+            "workload": "advdiff2d 64^2, one EXPRB2 Leja step, dt = 50 dt_CFL, tol 1e-10 "
+                        "(NumPy in/out, includes linearisation + power iteration)",
+            "us_per_call": t * 1e6}
+    # config 2: Allen-Cahn 256^2 EXPRB43, 100 adaptive steps, Leja / KIOPS
+    p = ext.allen_cahn_periodic_problem(n=256)
+    for scheme in ("leja", "kiops"):
+        t, tr = timed(lambda: ek.adaptive_loop(p.rhs, p.u0, 1.0, "exprb43", scheme, 1e-10,
+                                               ctx=ek.EngineContext(xi=xi), max_steps=100))
+        nst = tr.steps_accepted + tr.steps_rejected
+        out[f"config2_{scheme}"] = {
+            "workload": "allen_cahn_periodic 256^2, EXPRB43, FD Jv, tol 1e-10, 100 adaptive "
+                        "steps from dt_init = 1e-5",
+            "ms_per_step": t / nst * 1e3, "steps": nst, "t_reached": tr.t,
+            "rhs_evals": tr.rhs_evals, "leja_iters": tr.leja_iters,
+            "krylov_matvecs": tr.krylov_matvecs,
+            "jv_per_s": (tr.leja_iters + tr.krylov_matvecs) / t}
+    # config 3: Burgers 1024^2 EPIRK4s3, 20 adaptive steps, Leja / LeKry / KIOPS
+    p = ext.burgers2d_problem(n=1024)
+    for scheme in ("leja", "lekry", "kiops"):
+        t, tr = timed(lambda: ek.adaptive_loop(p.rhs, p.u0, 1.0, "epirk4s3", scheme, 1e-8,
+                                               jac_factory=p.jac_factory,
+                                               ctx=ek.EngineContext(xi=xi), max_steps=20))
+        nst = tr.steps_accepted + tr.steps_rejected
+        out[f"config3_{scheme}"] = {
+            "workload": "burgers2d 1024^2, EPIRK4s3, analytic Jv, tol 1e-8, 20 adaptive steps",
+            "ms_per_step": t / nst * 1e3, "steps": nst, "t_reached": tr.t,
+            "leja_iters": tr.leja_iters, "krylov_matvecs": tr.krylov_matvecs,
+            "jv_per_s": (tr.leja_iters + tr.krylov_matvecs) / t}
+    del p
+    # config 5: adv-diff 512^3, EXPRB32 Leja at fixed dt = 50 dt_CFL (3 steps)
+    if left() < 20.0:
+        out["config5"] = {"skipped": "bench configs time budget"}
+        return out
+    p = ext.advdiff3d_problem(n=512)
+    u0 = torch.from_numpy(p.u0).cuda()
+    dt = 50.0 * p.params["dt_cfl"]
+    steps = 3
+    rhs = ek.CountingRhs(p.rhs)
+    sys0 = ek.make_linearized(rhs, u0, jac_factory=p.jac_factory, _as_numpy=False)
+    est = ek.make_estimate(ek.power_iterate(sys0.J)[0])
+    del sys0
+
+    def run5():
+        ctx = ek.EngineContext(xi=xi, est=est)
+        u, it = u0, 0
+        for _ in range(steps):
+            s_ = ek.make_linearized(rhs, u, jac_factory=p.jac_factory, _as_numpy=False)
+            ctx.est = ek.maybe_refresh(ctx.est, s_.J, ek.RefreshPolicy())
+            r = ext.take_step_ext("exprb32", s_, dt, "leja", 1e-10, ctx)
+            u, it = r._u, it + r.stats.leja_iters
+        return it
+
+    run5()
+    torch.cuda.synchronize()
+    L.PROFILE = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    iters = run5()
+    e1.record()
+    torch.cuda.synchronize()
+    prof, L.PROFILE = L.PROFILE, None
+    el = e0.elapsed_time(e1) / 1e3
+    kb, kt = 0, 0.0
+    for q in prof:
+        kb += leja_bytes(q)[0]
+        kt += sum(a.elapsed_time(b) for a, b in q["events"]) / 1e3
+    peak, _ = peaks()
+    out["config5"] = {
+        "workload": "advdiff3d 512^3 (1.07 GB per vector), EXPRB32 Leja, linear analytic Jv, "
+                    "fixed dt = 50 dt_CFL, tol 1e-10, 3 steps (estimate precomputed)",
+        "ms_per_step": el / steps * 1e3, "leja_iters": iters,
+        "jv_per_s": (iters + steps) / el,
+        "leja_kernel": {"achieved_gbs": kb / kt / 1e9 if kt else None, "peak_gbs": peak,
+                        "frac": kb / kt / 1e9 / peak if kt else None,
+                        "bytes_model": "8*N*(2+2*k_active) per launch (linear Jv)",
+                        "share_of_step": kt / el}}
+    return out
+
+
 # ------------------------------------------------------------ CPU side
 
-def _oracle_setup(n):
-    from oracle import np_fields as OF, np_integrate as OI, np_phi as OP
-    q = OF.brusselator_periodic(n=n)
-    rhs = OP.CountedRhs(q.rhs)
-    sys_ = OI.linearize(rhs, q.u0)
-    return OP, sys_, rhs
+def reference_engines():
+    """The reference's own engines for the CPU legs: the unmodified
+    reference package installed under baseline/_ref (pure Python; it
+    travels with the repo snapshot, git-ignored) when present, else the
+    NumPy restatement in oracle/ (pinned bit-exact to it). Returns
+    (kind, namespace) with the engine calls the CPU legs need."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "expkit" / "integrators.py").exists():
+        if str(ref) not in sys.path:
+            sys.path.insert(0, str(ref))
+        try:
+            from expkit import integrators as RI, linalg as RL, spectrum as RS, leja as RLJ
+
+            class NS:
+                kind = "reference"
+                source = "baseline/_ref (the unmodified reference package expkit)"
+                CountingRhs = RL.CountingRhs
+                make_estimate = RS.make_estimate
+                leja_points = staticmethod(lambda: RLJ.get_leja_points(400))
+
+                @staticmethod
+                def linearize(rhs, u, jac_factory=None):
+                    return RI.make_linearized(rhs, u, jac_factory=jac_factory)
+
+                @staticmethod
+                def step(name, sys_, dt, scheme, tol, est, xi):
+                    return RI.take_step(name, sys_, dt, scheme, tol,
+                                        RI.EngineContext(est=est, xi=xi))
+            return NS
+        except ImportError:
+            pass
+    from oracle import np_integrate as OI, np_phi as OP
+
+    class NSP:
+        kind = "port"
+        source = "oracle/ (NumPy restatement of the reference, pinned bit-exact)"
+        CountingRhs = OP.CountedRhs
+        make_estimate = staticmethod(OP.estimate)
+        leja_points = staticmethod(lambda: OP.leja_points(400))
+
+        @staticmethod
+        def linearize(rhs, u, jac_factory=None):
+            return OI.linearize(rhs, u, jac_factory=jac_factory)
+
+        @staticmethod
+        def step(name, sys_, dt, scheme, tol, est, xi):
+            return OI.step(name, sys_, dt, scheme, tol, OI.Ctx(est=est, xi=xi))
+    return NSP
 
 
 def _limit_threads(k):
+    os.environ["OPENBLAS_NUM_THREADS"] = str(k)
     try:
         from threadpoolctl import threadpool_limits
         return threadpool_limits(limits=k)
@@ -365,27 +530,63 @@ def _limit_threads(k):
         return contextlib.nullcontext()
 
 
-def cpu_baseline(n, dt, iters=8):
-    """The oracle (NumPy restatement of the reference, pinned bit-exact) on
-    this host, 1 core: `iters` FD Leja iterations of the same workload."""
+def cpu_epirk5p1_steps(n, lam, steps, budget_s=None):
+    """Full EPIRK5P1 Leja steps of config 4 by the reference engines on one
+    host core (1 BLAS thread; numpy elementwise is single-threaded): the
+    same problem (oracle/np_fields' restatement of the periodic Brusselator
+    plugin, which the reference lacks), the same estimate and dt as the GPU
+    arm (lam = its power-iteration |lambda|), the same tolerance. Returns
+    (Jv, seconds, steps, kind, source). Linearisation of each step is timed
+    (it is part of the step, as in fixed_step_loop)."""
+    from oracle import np_fields as OF
+    R = reference_engines()
     with _limit_threads(1):
-        OP, sys_, rhs = _oracle_setup(n)
-        xi = OP.leja_points(400)
-        # the GPU run's stiffness window: alpha = -50/dt
-        est = OP.estimate(DT_ALPHA / dt / 1.1)
-        b = sys_.f_n * dt
-        c0 = rhs.counter.count
+        q = OF.brusselator_periodic(n=n)
+        xi = R.leja_points()
+        est = R.make_estimate(lam)
+        dt = DT_ALPHA / abs(est.alpha)
+        rhs = R.CountingRhs(q.rhs)
+        u = q.u0
+        jv, el, done = 0, 0.0, 0
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            sys_ = R.linearize(rhs, u)
+            res = R.step(INTEGRATOR, sys_, dt, "leja", TOL, est, xi)
+            el += time.perf_counter() - t0
+            u = res.u_high
+            jv += res.stats.leja_iters + res.stats.group_rhs_evals.get("remainder", 0) // 2
+            done += 1
+            if budget_s is not None and el > budget_s:
+                break
+    return jv, el, done, R.kind, R.source
+
+
+def cpu_config5_jv(budget=1):
+    """Per-Jv rate of config 5 (512^3 linear analytic Jacobian) by the
+    oracle's plugin RHS on one core (per-Jv rate only)."""
+    from oracle import np_fields as OF
+    with _limit_threads(1):
+        q = OF.advdiff3d(n=512)
+        v = q.u0
         t0 = time.perf_counter()
-        try:
-            OP.leja_vertical(sys_.J, b, 1, [1.0], dt, est, 1e-300, xi, max_points=iters + 1)
-        except OP.NonConvergence:
-            pass
+        for _ in range(budget):
+            v = q.rhs(v)
         el = time.perf_counter() - t0
-        jvs = rhs.counter.count - c0
-    return {"value": jvs / el, "unit": "Jv/s", "cores": 1, "kind": "port",
-            "sample": f"{jvs} FD Leja iterations (phi_1, k=1) of config 4 "
-                      f"({n}x{n}x2) by oracle/np_phi.leja_vertical, 1 BLAS thread",
-            "seconds": el, "host": _host_info()}
+    return budget / el
+
+
+def cpu_baseline(n, lam, with_c5=True):
+    """cpu_baseline of our arm: one full EPIRK5P1 step of the same workload
+    by the reference engines on one host core (~20-30 s)."""
+    jv, el, done, kind, source = cpu_epirk5p1_steps(n, lam, 1)
+    out = {"value": jv / el, "unit": "Jv/s", "cores": 1, "kind": kind,
+           "sample": f"{done} full EPIRK5P1 Leja step(s) of config 4 ({n}x{n}x2, dt|alpha| "
+                     f"= {DT_ALPHA:g}, tol {TOL:g}; {jv} Jacobian actions) by {source}, "
+                     "1 BLAS thread",
+           "ms_per_step": el / done * 1e3, "seconds": el, "host": _host_info()}
+    if with_c5:
+        out["config5_jv_per_s"] = cpu_config5_jv()
+    return out
 
 
 def _host_info():
@@ -397,61 +598,92 @@ def _host_info():
                 break
     except OSError:
         pass
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                info["lscpu_model"] = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
     import numpy
     import scipy
     info["numpy"] = numpy.__version__
     info["scipy"] = scipy.__version__
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [f"{d.get('internal_api')} {d.get('version')} "
+                        f"({d.get('threading_layer')})" for d in threadpool_info()
+                        if d.get("user_api") == "blas"]
+    except ImportError:
+        pass
     return info
 
 
 def run_reference(args, rank, world):
-    """Reference arm: the reference's algorithm on the host CPU (oracle
-    restatement), one FD Leja iteration per step, same config / metric."""
+    """Reference arm: the reference's engines (baseline/_ref, else the
+    pinned port) on the host CPU, one core (1 BLAS thread),
+    timing min(steps, 2) full EPIRK5P1 Leja steps of config 4 — the same
+    step, metric and dt rule as our arm. dt comes from the reference's own
+    power iteration of the same linearisation (untimed setup, as in our
+    arm). Under torchrun only rank 0 runs."""
     if rank != 0:
         return None
+    from oracle import np_fields as OF
     n = args.grid
-    OP, sys_, rhs = _oracle_setup(n)
-    xi = OP.leja_points(400)
-    # the same stiffness window as our arm: dt |alpha| = 50 with alpha from a
-    # short power iteration of the oracle
-    lam, _ = OP.power_iterate(sys_.J, max_it=8)
-    est = OP.estimate(lam)
-    dt = DT_ALPHA / abs(est.alpha)
-    b = sys_.f_n * dt
-    if args.warmup > 0:
-        try:
-            OP.leja_vertical(sys_.J, b, 1, [1.0], dt, est, 1e-300, xi, max_points=2)
-        except OP.NonConvergence:
-            pass
-    c0 = rhs.counter.count
-    t0 = time.perf_counter()
-    try:
-        OP.leja_vertical(sys_.J, b, 1, [1.0], dt, est, 1e-300, xi,
-                         max_points=args.steps + 1)
-    except OP.NonConvergence:
-        pass
-    el = time.perf_counter() - t0
-    jvs = rhs.counter.count - c0
-    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
-    val = jvs / el
+    R = reference_engines()
+    with _limit_threads(1):
+        q = OF.brusselator_periodic(n=n)
+        if R.kind == "reference":
+            from expkit import spectrum as RS
+            lam, _ = RS.power_iterate(R.linearize(R.CountingRhs(q.rhs), q.u0).J)
+        else:
+            from oracle import np_phi as OP
+            lam, _ = OP.power_iterate(R.linearize(R.CountingRhs(q.rhs), q.u0).J)
+        del q
+    steps = max(1, min(args.steps, 2))
+    jv, el, done, kind, source = cpu_epirk5p1_steps(n, lam, steps)
+    val = jv / el
+    dt = DT_ALPHA / abs(R.make_estimate(lam).alpha)
     return {"impl": "reference", "metric": METRIC, "value": val, "unit": "Jv/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": el / max(jvs, 1) * 1e3, "higher_is_better": True,
+            "n_gpus": world, "steps": done, "warmup": 0,
+            "ms_per_step": el / done * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded smooth perturbation of the Brusselator steady state",
-            "config": config_dict(n, dt, {"step": "one FD Leja iteration (bounded sample)"}),
-            "cpu_baseline": {"value": val, "unit": "Jv/s", "cores": 1, "kind": "port",
-                             "sample": f"{jvs} FD Leja iterations of config 4 by the "
-                                       "NumPy oracle (numpy elementwise is single-"
-                                       f"threaded; BLAS threads {threads})",
+            "config": config_dict(n, dt, {
+                "step": "one full EPIRK5P1 Leja step (linearise + take_step), as our arm",
+                "timed_steps": f"min(--steps, 2) = {done} (CPU steps take ~20-30 s each); "
+                               "no warm-up (NumPy has nothing to warm)"}),
+            "cpu_baseline": {"value": val, "unit": "Jv/s", "cores": 1, "kind": kind,
+                             "sample": f"{done} EPIRK5P1 steps ({jv} Jacobian actions) by "
+                                       f"{source}; plugin RHS from oracle/np_fields; "
+                                       "1 BLAS thread (numpy elementwise is single-threaded)",
                              "host": _host_info()},
             "e2e": {"value": val, "unit": "Jv/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
+def spawn(n):
+    """`bench.py --gpus N` without a launcher: re-exec under
+    torch.distributed.run with N ranks on this node (127.0.0.1), the same
+    command form the driver uses; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args.gpus))
     rank, world, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} ranks",
+              file=sys.stderr)
     if args.impl == "reference":
         out = run_reference(args, rank, world)
     else:
