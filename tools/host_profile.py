@@ -1,41 +1,54 @@
 #!/usr/bin/env python
-"""cProfile of a small-grid adaptive run (host-overhead analysis).
+"""Host-side profile of a small-grid adaptive run (where the per-step time
+goes when the device work is microseconds): cProfile of one run after a
+warm-up, top functions by internal and cumulative time.
 
-    python tools/host_profile.py [problem n integrator scheme steps]
+    python tools/host_profile.py c3_leja > hp.txt
 """
-import cProfile, pstats, sys, time
+
+import cProfile
+import pstats
+import sys
+import time
 from pathlib import Path
+
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import paper_2211_08948_b200 as ek
-from paper_2211_08948_b200 import ext
-
-a = sys.argv[1:]
-name = a[0] if a else "allen_cahn_periodic"
-n = int(a[1]) if len(a) > 1 else 256
-integ = a[2] if len(a) > 2 else "exprb43"
-scheme = a[3] if len(a) > 3 else "leja"
-steps = int(a[4]) if len(a) > 4 else 100
-p = ext.make_ext_problem(name, n=n)
-xi = ek.get_leja_points(400)
 
 
-def run():
-    return ek.adaptive_loop(p.rhs, p.u0, 1.0, integ, scheme, 1e-10 if name != "burgers2d" else 1e-8,
-                            jac_factory=p.jac_factory, ctx=ek.EngineContext(xi=xi),
-                            max_steps=steps)
+def main():
+    which = sys.argv[1] if len(sys.argv) > 1 else "c3_leja"
+    import torch
+    import paper_2211_08948_b200 as ek
+    from paper_2211_08948_b200 import ext
+    xi = ek.get_leja_points(400)
+    cfg, scheme = which.split("_")
+    if cfg == "c2":
+        p = ext.allen_cahn_periodic_problem(n=256)
+        run = lambda: ek.adaptive_loop(p.rhs, p.u0, 1.0, "exprb43", scheme, 1e-10,
+                                       ctx=ek.EngineContext(xi=xi), max_steps=100)
+    else:
+        p = ext.burgers2d_problem(n=1024)
+        run = lambda: ek.adaptive_loop(p.rhs, p.u0, 1.0, "epirk4s3", scheme, 1e-8,
+                                       jac_factory=p.jac_factory,
+                                       ctx=ek.EngineContext(xi=xi), max_steps=20)
+    run()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tr = run()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    nst = tr.steps_accepted + tr.steps_rejected
+    print(f"{which}: {nst} steps in {el:.4f} s ({el / nst * 1e3:.3f} ms/step), "
+          f"leja {tr.leja_iters}, krylov {tr.krylov_matvecs}")
+    pr = cProfile.Profile()
+    pr.enable()
+    run()
+    torch.cuda.synchronize()
+    pr.disable()
+    st = pstats.Stats(pr, stream=sys.stdout)
+    st.sort_stats("tottime").print_stats(35)
+    st.sort_stats("cumulative").print_stats(45)
 
 
-run()
-t0 = time.perf_counter()
-tr = run()
-t1 = time.perf_counter()
-print(f"{name} {n} {integ} {scheme}: {steps} steps in {t1 - t0:.3f} s "
-      f"({(t1 - t0) / steps * 1e3:.2f} ms/step), rhs {tr.rhs_evals}, leja {tr.leja_iters}, "
-      f"krylov {tr.krylov_matvecs}")
-pr = cProfile.Profile()
-pr.enable()
-run()
-pr.disable()
-st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(30)
-st.sort_stats("cumulative").print_stats(40)
+if __name__ == "__main__":
+    main()
