@@ -190,10 +190,40 @@ def clear_checks():
     _PENDING.clear()
 
 
+_PIN = [None]
+
+
+def _pull_all(states):
+    """Read several state blocks with ONE stream synchronisation: async
+    copies into a pinned staging buffer, one sync, then host copies."""
+    sizes = [(s.size + 15) // 16 * 16 for s in states]
+    total = sum(sizes)
+    buf = _PIN[0]
+    if buf is None or buf.numel() < total:
+        buf = torch.empty(max(total, 1 << 16), dtype=torch.uint8, pin_memory=True)
+        _PIN[0] = buf
+    base, off, strm = buf.data_ptr(), 0, stream()
+    for st, sz in zip(states, sizes):
+        N.check(N.lib().ek_copy(C.c_void_p(base + off), st.ptr, st.size, 2, strm),
+                "state read")
+        off += sz
+    N.check(N.lib().ek_sync(strm), "state sync")
+    off = 0
+    for st, sz in zip(states, sizes):
+        C.memmove(C.addressof(st.host), base + off, st.size)
+        off += sz
+
+
 def flush_checks():
+    if len(_PENDING) > 1:
+        uniq = list({id(st): st for st, _, _ in _PENDING}.values())
+        _pull_all(uniq)
+        fresh = {id(st) for st in uniq}
+    else:
+        fresh = ()
     while _PENDING:
         st, mask, fn = _PENDING.pop(0)
-        h = st._pull()
+        h = st.host if id(st) in fresh else st._pull()
         if mask is None:
             fn(h)
         elif h.flag & mask:

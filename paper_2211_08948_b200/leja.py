@@ -244,9 +244,15 @@ def _slab_decide(st, Jn, table, base, m, k, begin):
     return gathered
 
 
+class SpecMiss(Exception):
+    """A speculative phi-call (see `leja_interpolate_vertical` _spec) did
+    not finish inside its launch batch, or stopped on an error status: the
+    step that used its vectors must be recomputed without speculation."""
+
+
 def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                               xi=None, max_points=DEFAULT_NUM_POINTS, _lazy_m0=False,
-                              _first_batch=8):
+                              _first_batch=8, _spec=None, _spec_zero=False):
     """phi_l(c_i h J) b for several scale factors c_i sharing one Newton
     basis recurrence (leja.py:133-189). Accumulator i freezes once
     |d_i[m]| ||y_m|| < tol; the loop runs until all are frozen.
@@ -261,7 +267,23 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     _lazy_m0 (integrator engines only, device b): if every accumulator
     freezes at m = 0 the results d_i[0]*b are returned as expressions
     (`_device.Expr`) that the stage algebra evaluates in registers with the
-    same rounding, instead of being written to HBM."""
+    same rounding, instead of being written to HBM.
+
+    _spec (integrator engines only, fused single-GPU path): speculative call.
+    The begin pass and ONE launch batch of `_first_batch` iterations are
+    enqueued and the accumulators are returned at once, without a host
+    synchronisation; the termination test already runs on the device (the
+    kernels after termination early-exit), so the vectors are final if the
+    call finished inside the batch. `_spec(iters, freeze_iters, fd_evals)`
+    is called when the state block is read at the stream's next host sync
+    (`_device.flush_checks`, in program order); if the call did not finish
+    in the batch, or stopped on an error status, that read raises SpecMiss
+    and the engines' caller recomputes the step without speculation
+    (integrators.run_stepper), so results, counters and exceptions are
+    those of the synchronous path. _spec_zero: the engines predict that
+    every accumulator freezes at m = 0 (it did last time for this group);
+    only the begin pass is enqueued and the results are the lazy
+    expressions d_i[0]*b — the read checks iters == 0."""
     if tol <= 0:
         raise ValueError("tolerance must be positive")
     if len(coeffs) < 1:
@@ -307,7 +329,9 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     # fused single-GPU path: the begin pass only takes ||b|| and the m = 0
     # decisions; the first iteration writes p_i = d_i[0] b + d_i[1] y_1
     fold = Jn is not None and not slab and max_points > 1
-    lazy = bool(_lazy_m0 and fold and isinstance(b, torch.Tensor))
+    spec = _spec is not None and fold and min(_CHUNK, max_points) > int(_first_batch)
+    spec_zero = spec and _spec_zero and _lazy_m0 and isinstance(b, torch.Tensor)
+    lazy = bool(_lazy_m0 and fold and (spec_zero or not spec) and isinstance(b, torch.Tensor))
     st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k, defer=1 if slab else 0,
                     p_init=-1 if fold else 0, lazy0=1 if lazy else 0)
     if nu_dev is not None:
@@ -329,6 +353,14 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                               freeze_iters=[0] * k)
     # fused path: the first launch batch follows without a host round trip;
     # its kernels early-exit if everything froze at m = 0
+    if spec_zero:
+        def on_begin(hst):
+            if hst.status != N.ST_OK or not hst.done or int(hst.iters) != 0:
+                raise SpecMiss("phi-call predicted to stop at m = 0 did not")
+            _spec(0, [0] * k, 0)
+        D.defer_fn(st, on_begin)
+        return LejaResult(vectors=[float(dds[i][0]) * D.V(bd) for i in range(k)],
+                          iters=None, freeze_iters=None)
 
     ybuf = [D.empty(n), D.empty(n)]
     yp = N.ptrs(ybuf)
@@ -386,6 +418,17 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             if prof is not None:
                 ev[1].record()
                 prof["events"].append(ev)
+            if spec:
+                def on_state(hst, prof=prof):
+                    if hst.status != N.ST_OK or not hst.done:
+                        raise SpecMiss("phi-call did not finish in its launch batch")
+                    iters = int(hst.iters)
+                    freeze = [int(hst.freeze[i]) for i in range(k)]
+                    if prof is not None:
+                        prof["iters"], prof["freeze"] = iters, freeze
+                    _spec(iters, freeze, int(hst.fd_evals) if Jn.jac == N.JAC_FD else 0)
+                D.defer_fn(st, on_state)
+                return LejaResult(vectors=ps, iters=None, freeze_iters=None)
             if hi == m_avail < max_points:
                 # the next chunk's tables start in the
                 # worker pool while this batch runs on the device

@@ -81,3 +81,11 @@ for lim in (5, 20, 50, 100, 1000):
     print(f"  gaps >= {lim:5d} us: {len(sel):4d}, {sum(sel)/1e3:.3f} ms")
 for g, name in gaps[:12]:
     print(f"  {g:9.1f} us before {name[:90]}")
+by = {}
+for s, e, name in iv:
+    key = name[:70]
+    c, t = by.get(key, (0, 0.0))
+    by[key] = (c + 1, t + (e - s))
+print("device time by kernel (per step):")
+for key, (c, t) in sorted(by.items(), key=lambda kv: -kv[1][1])[:16]:
+    print(f"  {t / K / 1e3:8.3f} ms  {c / K:6.1f} x  {key}")
