@@ -377,6 +377,9 @@ def secondary_configs(ek, xi, budget_s=120.0):
     def timed(run, reps=1):
         run()
         torch.cuda.synchronize()
+        # honest adaptive windows: the warm-up run's divided-difference
+        # tables (same dt sequence) must not serve the timed run
+        L._DD_CACHE.clear()
         t0 = time.perf_counter()
         for _ in range(reps):
             r = run()

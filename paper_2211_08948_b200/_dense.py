@@ -13,6 +13,11 @@ import math
 import numpy as np
 import scipy.linalg
 
+try:  # the compiled routine behind scipy.linalg.expm (same bits, batched)
+    from scipy.linalg._matfuncs import matrix_exponential as _matrix_exponential
+except ImportError:  # pragma: no cover - other scipy layouts
+    _matrix_exponential = None
+
 def dense_expm(M):
     """exp(M) of a small dense matrix by scipy's Pade scaling-and-squaring
     (linalg.py:132-139) — the same function the reference calls."""
@@ -84,3 +89,43 @@ def phi_divided_differences(l, h, c, gamma, xi, m):
     e1 = np.zeros(m)
     e1[0] = 1.0
     return dense_phi_action(l, L, e1)
+
+
+def phi_divided_differences_many(l, hs, c, gamma, xi, m):
+    """phi_divided_differences for several scales h sharing l, c, gamma and
+    xi (one vertical Leja group): the augmented matrices of
+    `dense_phi_action` are stacked and exponentiated in ONE call of the
+    routine scipy.linalg.expm runs (it treats a stack slice by slice, so
+    every table has the bits of its own call — checked in
+    tests/test_host.py). Tables whose matrix takes another branch of
+    `dense_phi_action` (tiny norm: Taylor series; non-finite entries: the
+    error path) are computed one by one as before."""
+    hs = [float(h) for h in hs]
+    if _matrix_exponential is None or len(hs) < 2 or l < 0:
+        return [phi_divided_differences(l, h, c, gamma, xi, m) for h in hs]
+    x = np.asarray(xi[:m], dtype=np.float64)
+    r = np.arange(m - 1)
+    n = m + l if l > 0 else m
+    stack = np.zeros((len(hs), n, n))
+    batch, out = [], [None] * len(hs)
+    for i, h in enumerate(hs):
+        L = np.diag(h * (c + gamma * x))
+        L[r + 1, r] = h * gamma
+        if not np.isfinite(L).all() or (l > 0 and np.linalg.norm(L) < 1e-8):
+            out[i] = phi_divided_differences(l, h, c, gamma, xi, m)
+            continue
+        a = stack[len(batch)]
+        a[:m, :m] = L
+        if l > 0:
+            a[0, m] = 1.0                     # aug[:n, n] = b = e_1
+            idx = np.arange(l - 1)
+            a[m + idx, m + idx + 1] = 1.0
+        batch.append(i)
+    if batch:
+        E, info = _matrix_exponential(stack[:len(batch)])
+        if info != 0:
+            return [phi_divided_differences(l, h, c, gamma, xi, m) for h in hs]
+        for j, i in enumerate(batch):
+            # dense_phi_action: (expm(aug) @ e_last)[:m]; l = 0: expm(L) @ e_1
+            out[i] = E[j][:m, -1].copy() if l > 0 else E[j][:m, 0].copy()
+    return out

@@ -131,15 +131,17 @@ def work_ptr(nbytes=None):
 class DevState:
     """A ctypes Structure mirrored in device memory."""
 
-    def __init__(self, ctype, **init):
+    def __init__(self, ctype, upload=True, **init):
         self.ctype = ctype
         self.size = C.sizeof(ctype)
-        # fully initialised by the upload below (no fill kernel)
+        # fully initialised by the upload below (no fill kernel), or by a
+        # device init kernel of the caller (upload=False)
         self.buf = torch.empty(self.size, dtype=torch.uint8, device=device())
         self.host = ctype()
         for k, v in init.items():
             setattr(self.host, k, v)
-        self.upload()
+        if upload:
+            self.upload()
 
     @property
     def ptr(self):

@@ -101,6 +101,8 @@ _SIGS = {
                                     C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), _P, _P, _PP,
                                     _P]),
     "ek_leja_begin_len": (_I, [_L, _P, _PP, _I, _P, _P, _P, _P]),
+    "ek_leja_call": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _P, _D, _D, _P,
+                          _I, _I, _I, _D, _P, _P, _P]),
     "ek_leja_run": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
                          _I, _I, _D, _P, _P, _PP, _P]),
     "ek_leja_update": (_I, [_L, _P, _P, _P, _PP, _I, _P, _I, _I, _D, _I, _P,

@@ -128,6 +128,21 @@ struct LejaVArgs {
     double* work;
 };
 
+// Initialise a Leja state block on the device (ek_leja_call): the host
+// values travel as kernel arguments, ||u|| optionally from a device slot.
+__global__ void k_leja_init(ek_leja_state* st, double tol, double nu, const double* nu_dev,
+                            int k, int p_init, int lazy0) {
+    if (threadIdx.x == 0) {
+        ek_leja_state z{};
+        z.tol = tol;
+        z.nu = nu_dev ? *nu_dev : nu;
+        z.k = k;
+        z.p_init = p_init;
+        z.lazy0 = lazy0;
+        *st = z;
+    }
+}
+
 // m = 0 of the Newton-Leja sum (leja.py:159-165).
 __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
     // fold request (host set p_init = -1): leave p to the first iteration.

@@ -436,6 +436,28 @@ int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu, co
     return EK_OK;
 }
 
+int ek_leja_call(const ek_grid* g, int jac, const double* u, const double* fu, const double* b,
+                 double* const* ybuf, double* const* p, int k, const double* coef_host,
+                 double* coef_dev, double tol, double nu, const double* nu_dev, int fold,
+                 int lazy0, int m_end, double gamma, ek_leja_state* st, double* work,
+                 void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (k < 1 || k > 8 || !coef_host || !coef_dev || !st) {
+        set_error("ek_leja_call: bad arguments (k=%d)", k);
+        return EK_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(coef_dev, coef_host, (size_t)(k + 1) * 32 * sizeof(double),
+                                    cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "ek_leja_call");
+    k_leja_init<<<1, 32, 0, s>>>(st, tol, nu, nu_dev, k, fold ? -1 : 0, lazy0);
+    EK_LAUNCH_CHECK("k_leja_init");
+    int rc = ek_leja_begin_len(ek_grid_len(g), b, p, k, coef_dev, st, work, stream);
+    if (rc != EK_OK || m_end <= 1) return rc;
+    return ek_leja_run(g, jac, u, fu, b, ybuf, p, k, coef_dev, 0, 1, m_end, gamma, st, work,
+                       nullptr, stream);
+}
+
 int ek_leja_update(int64_t len, const double* jv, const double* y, double* ynext,
                    double* const* p, int k, const double* coef_dev, int chunk_base, int m,
                    double gamma, int check_jv, ek_leja_state* st, double* work, void* stream) {

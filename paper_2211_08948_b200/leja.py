@@ -29,7 +29,7 @@ from . import _ddpool
 from . import _device as D
 from . import _native as N
 from .errors import NonConvergence
-from ._dense import phi_divided_differences
+from ._dense import phi_divided_differences, phi_divided_differences_many
 from .linalg import MatrixFreeOperator, fused_target
 from .spectrum import SpectrumEstimate
 
@@ -43,6 +43,7 @@ _cached_points = None
 # appends {"events": [(start, end), ...], "iters", "freeze", "k", "n", "fd"}
 # with CUDA events bracketing its ek_leja_run launch batches.
 PROFILE = None
+_FASTCALL = os.environ.get("EK_LEJA_FASTCALL", "1") != "0"  # A/B switch (tools)
 
 
 def generate_leja_points(m=DEFAULT_NUM_POINTS, n_candidates=DEFAULT_CANDIDATES):
@@ -165,6 +166,22 @@ def _dd_cached(l, h, est, xi, m_max):
     return d
 
 
+def _dd_group(l, hs, est, xi, m_max):
+    """_dd_cached for the scales of one vertical group: first-chunk tables
+    that miss the memo are computed in one batched exponential call
+    (`_dense.phi_divided_differences_many`, the same bits per table)."""
+    m = min(m_max, len(xi))
+    keys = [_dd_key(l, h, est, xi, m_max) for h in hs]
+    miss = [i for i, k in enumerate(keys) if k not in _DD_CACHE]
+    if len(miss) > 1 and m <= _CHUNK and 0 <= l <= 4 and min(hs) >= 0:
+        ds = phi_divided_differences_many(l, [hs[i] for i in miss], est.c, est.gamma, xi, m)
+        for i, d in zip(miss, ds):
+            if not np.isfinite(d).all():  # as divided_differences()
+                raise NonConvergence("non-finite divided differences; spectral estimate invalid")
+            _dd_store(keys[i], d)
+    return [_dd_cached(l, h, est, xi, m_max) for h in hs]
+
+
 def _one_blas_thread():
     """In-process fallback for large tables: the pool's one-thread BLAS."""
     try:
@@ -216,6 +233,16 @@ class _CoefTable:
         self.host = np.zeros((k + 1) * _CHUNK)
 
     def load(self, base, hi, dds, c, gamma, xi):
+        self.fill(base, hi, dds, c, gamma, xi)
+        self.upload()
+
+    def upload(self):
+        h = self.host
+        N.check(N.lib().ek_copy(C.c_void_p(self.dev.data_ptr()),
+                                h.ctypes.data_as(C.c_void_p), h.nbytes, 1, D.stream()),
+                "coef upload")
+
+    def fill(self, base, hi, dds, c, gamma, xi):
         h = self.host
         h[:] = 0.0
         lo = max(base, 1)
@@ -223,9 +250,6 @@ class _CoefTable:
             h[lo - base:hi - base] = (c / gamma) + np.asarray(xi[lo - 1:hi - 1], dtype=np.float64)
         for i, d in enumerate(dds):
             h[(1 + i) * _CHUNK:(1 + i) * _CHUNK + (hi - base)] = d[base:hi]
-        N.check(N.lib().ek_copy(C.c_void_p(self.dev.data_ptr()),
-                                h.ctypes.data_as(C.c_void_p), h.nbytes, 1, D.stream()),
-                "coef upload")
 
 
 def _part_view(st):
@@ -309,9 +333,9 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     for mm in range(2 * _CHUNK, ahead + 1, _CHUNK):
         for ci in coeffs:
             _dd_prefetch(l, ci * h, est, xi, mm)
-    dds = [_dd_cached(l, ci * h, est, xi, m_avail) for ci in coeffs]
+    dds = _dd_group(l, [ci * h for ci in coeffs], est, xi, m_avail)
     table = _CoefTable(k)
-    table.load(0, min(_CHUNK, m_avail), dds, c, gamma, xi)
+    table.fill(0, min(_CHUNK, m_avail), dds, c, gamma, xi)
 
     fused = fused_target(J)
     if fused is not None and (fused[1] != 1.0 or fused[0].grid.problem == N.P_SEMILINEAR):
@@ -332,17 +356,32 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     spec = _spec is not None and fold and min(_CHUNK, max_points) > int(_first_batch)
     spec_zero = spec and _spec_zero and _lazy_m0 and isinstance(b, torch.Tensor)
     lazy = bool(_lazy_m0 and fold and (spec_zero or not spec) and isinstance(b, torch.Tensor))
-    st = D.DevState(N.LejaState, tol=float(tol), nu=nu, k=k, defer=1 if slab else 0,
-                    p_init=-1 if fold else 0, lazy0=1 if lazy else 0)
-    if nu_dev is not None:
-        N.check(N.lib().ek_copy(C.c_void_p(st.buf.data_ptr() + N.LejaState.nu.offset),
-                                C.c_void_p(nu_dev.buf.data_ptr() + N.ScalarState.val.offset + 8),
-                                8, 3, D.stream()), "nu copy")
+    # whole-grid fused call without profiling: table upload, state init,
+    # begin pass and the first launch batch in ONE native call
+    fast = fold and PROFILE is None and _FASTCALL
+    first_hi = min(m_avail, 1 + max(1, int(_first_batch)))
+    st = D.DevState(N.LejaState, upload=not fast, tol=float(tol), nu=nu, k=k,
+                    defer=1 if slab else 0, p_init=-1 if fold else 0, lazy0=1 if lazy else 0)
+    nu_ptr = None if nu_dev is None else \
+        C.c_void_p(nu_dev.buf.data_ptr() + N.ScalarState.val.offset + 8)
     ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(Jn.grid)) if Jn else None)
     pp = N.ptrs(ps)
-    N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()), pp, k,
-                                      C.c_void_p(table.dev.data_ptr()), st.ptr, ws,
-                                      D.stream()), "ek_leja_begin_len")
+    ybuf = None
+    if fast:
+        ybuf = None if spec_zero else [D.empty(n), D.empty(n)]
+        N.check(N.lib().ek_leja_call(
+            C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()), C.c_void_p(Jn.fu.data_ptr()),
+            C.c_void_p(bd.data_ptr()), N.ptrs(ybuf or []), pp, k, table.host.ctypes.data_as(C.c_void_p),
+            C.c_void_p(table.dev.data_ptr()), float(tol), nu, nu_ptr, 1, 1 if lazy else 0,
+            1 if spec_zero else first_hi, float(gamma), st.ptr, ws, D.stream()), "ek_leja_call")
+    else:
+        table.upload()
+        if nu_ptr is not None:
+            N.check(N.lib().ek_copy(C.c_void_p(st.buf.data_ptr() + N.LejaState.nu.offset),
+                                    nu_ptr, 8, 3, D.stream()), "nu copy")
+        N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()), pp, k,
+                                          C.c_void_p(table.dev.data_ptr()), st.ptr, ws,
+                                          D.stream()), "ek_leja_begin_len")
     if slab:
         _slab_decide(st, Jn, table, 0, 0, k, begin=True)
     if Jn is None or max_points <= 1:
@@ -362,7 +401,8 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
         return LejaResult(vectors=[float(dds[i][0]) * D.V(bd) for i in range(k)],
                           iters=None, freeze_iters=None)
 
-    ybuf = [D.empty(n), D.empty(n)]
+    if ybuf is None:
+        ybuf = [D.empty(n), D.empty(n)]
     yp = N.ptrs(ybuf)
     fd_seen = 0
     m = 1
@@ -382,11 +422,13 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
         if Jn is not None:
             # launch batch: short first batch (most calls finish early), then
             # the rest of the chunk; kernels after termination early-exit
-            hi = min(m_avail, m + max(1, int(_first_batch))) if m == 1 else m_avail
+            hi = first_hi if m == 1 else m_avail
             if prof is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
-            if slab and Jn.comm.peer:
+            if fast and m == 1:
+                pass  # launched by ek_leja_call
+            elif slab and Jn.comm.peer:
                 # peer mode: ghost rows of b once (NCCL), then every pass
                 # stores its boundary rows into the neighbours' windows and
                 # a decide kernel waits for the pass flags: no host work
