@@ -329,7 +329,7 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
             auto kern = k_tma3d<P, EV, EP, K, S>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, T3, SMEM) !=
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT3, SMEM) !=
                         cudaSuccess || tocc < 1)
                     tocc = 1;
             }
@@ -338,7 +338,7 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
                                   ((a.g.rows + SEG3 - 1) / SEG3);
             const int64_t cap = (int64_t)sm_count() * tocc;
             const unsigned grid = (unsigned)(items < cap ? items : cap);
-            kern<<<grid, T3, SMEM, s>>>(a, maps);
+            kern<<<grid, NT3, SMEM, s>>>(a, maps);
             EK_LAUNCH_CHECK("tma3 stencil launch");
             return EK_OK;
         }

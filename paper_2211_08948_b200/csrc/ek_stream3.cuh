@@ -62,7 +62,11 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
 #ifndef EK_MAP3_FLAT
 #define EK_MAP3_FLAT 0
 #endif
+#ifndef EK_PROD3
+#define EK_PROD3 1  // 1: one extra producer warp issues the plane copies
+#endif
 constexpr int T3 = EK_T3, NW3 = T3 / 32;
+constexpr int NT3 = T3 + (EK_PROD3 ? 32 : 0);  // threads per block
 constexpr int I3X = 64;
 constexpr int TBW3 = I3X + 4;
 __host__ __device__ constexpr int raw3(int iy) { return (TBW3 * (iy + 2) + 15) / 16 * 16; }
@@ -246,7 +250,7 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
 
 
 template <class P, int EV, int EP, int K, int S>
-__global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
     static_assert(S >= 4, "plane ring needs i-1, i, i+1 and one in flight");
     constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
     constexpr int NR = nraw<EV>();
@@ -255,7 +259,11 @@ __global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __gri
     static_assert(PPT >= 1 && PPT * T3 == IY * I3X, "item points must split evenly");
     extern __shared__ __align__(1024) double smem[];
     __shared__ __align__(8) uint64_t full[S];
+#if EK_PROD3
+    __shared__ __align__(8) uint64_t empty[S];  // the NW3 compute warps released stage s
+#else
     __shared__ int released[S];  // warps that released stage s, cumulative
+#endif
 
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
@@ -284,20 +292,50 @@ __global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __gri
             asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&maps.m[t]) : "memory");
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
+#if EK_PROD3
+            mbar_init(&empty[s], NW3);
+#else
             released[s] = 0;
+#endif
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#if !EK_PROD3
         // fill the ring: sequence numbers 0 .. S-1
         if (blockIdx.x < nitems) {
             const Item3 it0 = item3<IY>(blockIdx.x, n, rows);
             for (int s = 0; s < S; ++s) issue_ahead(blockIdx.x, it0, s - S, s);
         }
+#endif
     }
     __syncthreads();
 
     double acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+
+#if EK_PROD3
+    // Producer warp (the last one): issues every plane of this block's items
+    // in sequence order, each into its ring stage as soon as the NW3 compute
+    // warps have released the stage's previous plane. The compute warps only
+    // wait for the copies they consume and arrive on empty[] when done.
+    if ((int)(threadIdx.x >> 5) == NW3) {
+        if (lane == 0) {
+            long q = 0;
+            for (long t = blockIdx.x; t < nitems; t += G) {
+                const Item3 it = item3<IY>(t, n, rows);
+                for (int pos = 0; pos < it.L + 2; ++pos, ++q) {
+                    const int s = (int)(q % S);
+                    if (q >= S) mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
+                    issue_plane<EV, EP, NC, K>(a, maps, smem + s * SD, &full[s], it, pos, rows,
+                                               ctr_mask(ctl));
+                }
+            }
+        }
+        __syncwarp();
+        reduce_and_finalize<EV, EP, NQ, NT3>(a, acc);
+        return;
+    }
+#endif
 
     auto wait_full = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
     // This warp is done with sequence number q (position pos of item t). The
@@ -310,7 +348,12 @@ __global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __gri
             // (their values were consumed above), so no fence is needed
             // before the copy engine may overwrite it
             const int s = q % S;
+#if EK_PROD3
+            (void)t; (void)it; (void)pos;
+            mbar_arrive(&empty[s]);
+#else
             if ((atomicAdd(&released[s], 1) + 1) % NW3 == 0) issue_ahead(t, it, pos, s);
+#endif
         }
     };
 
@@ -388,7 +431,7 @@ __global__ void __launch_bounds__(T3, EK_LB3) k_tma3d(const KArgs a, const __gri
         release(q0 + it.L + 1, t, it, it.L + 1);
         q0 += it.L + 2;
     }
-    reduce_and_finalize<EV, EP, NQ, T3>(a, acc);
+    reduce_and_finalize<EV, EP, NQ, NT3>(a, acc);
 }
 
 }  // namespace ek
