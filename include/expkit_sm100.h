@@ -348,6 +348,19 @@ int ek_leja_run_peer(const ek_grid* g, int jac, const double* u, const double* f
                      const double* const* halo_b, const ek_peer* peer, double* win_local,
                      int64_t epoch0, void* stream);
 
+/* ek_leja_run_peer split by phase: 1 = the fused passes only (halo rows
+ * and partial sums stored into the peers' windows, pass flags raised),
+ * 2 = the decide kernels only, 3 = both (= ek_leja_run_peer). With fewer
+ * GPUs than ranks, a test drives every rank's pass of iteration m before
+ * any rank's decide kernel, all on one stream, so no kernel ever waits for
+ * one that has not been launched (tests/test_peer_emulated.py). */
+int ek_leja_run_peer_phase(const ek_grid* g, int jac, const double* u, const double* fu,
+                           const double* b, double* const* ybuf, double* const* p, int k,
+                           const double* coef_dev, int chunk_base, int m_begin, int m_end,
+                           double gamma, ek_leja_state* st, double* work,
+                           const double* const* halo_b, const ek_peer* peer,
+                           double* win_local, int64_t epoch0, int phase, void* stream);
+
 /* --------------------------------------------------- KIOPS (kiops.py) */
 /* V[0] = [src ; tail], beta = ||V[0]||, V[0] /= beta, ||V[0,:n]||
  * (kiops.py:168-177). Rows of V are device pointers of length n+p. */

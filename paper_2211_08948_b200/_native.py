@@ -119,6 +119,8 @@ _SIGS = {
     "ek_ipc_free": (_I, [_P]),
     "ek_leja_run_peer": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
                               _I, _I, _D, _P, _P, _PP, _P, _P, _L, _P]),
+    "ek_leja_run_peer_phase": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
+                                    _I, _I, _D, _P, _P, _PP, _P, _P, _L, _I, _P]),
     "ek_arnoldi_init": (_I, [_L, _I, _P, C.POINTER(_D), _P, _P, _P, _P]),
     "ek_arnoldi_run": (_I, [C.POINTER(Grid), _I, _P, _P, _PP, _PP,
                             C.POINTER(_I), _I, _D, _I, _I, _P, _P, _I, _I, _I,

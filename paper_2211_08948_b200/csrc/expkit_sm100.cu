@@ -536,6 +536,12 @@ int ek_power_decide(ek_power_state* st, const double* gathered, int nranks, int 
 }
 
 // --------------------------------------- slab mode over NVLink peer memory
+int ek_leja_run_peer_phase(const ek_grid* g, int jac, const double* u, const double* fu,
+                           const double* b, double* const* ybuf, double* const* p, int k,
+                           const double* coef_dev, int chunk_base, int m_begin, int m_end,
+                           double gamma, ek_leja_state* st, double* work,
+                           const double* const* halo_b, const ek_peer* peer,
+                           double* win_local, int64_t epoch0, int phase, void* stream);
 int64_t ek_peer_window_bytes(const ek_grid* g) {
     if (!grid_ok(g) || g->dim < 2) return 0;
     const int64_t rowlen = g->dim == 2 ? g->n : g->n * g->n;
@@ -581,6 +587,21 @@ int ek_leja_run_peer(const ek_grid* g, int jac, const double* u, const double* f
                      double gamma, ek_leja_state* st, double* work,
                      const double* const* halo_b, const ek_peer* peer, double* win_local,
                      int64_t epoch0, void* stream) {
+    return ek_leja_run_peer_phase(g, jac, u, fu, b, ybuf, p, k, coef_dev, chunk_base, m_begin,
+                                  m_end, gamma, st, work, halo_b, peer, win_local, epoch0, 3,
+                                  stream);
+}
+
+int ek_leja_run_peer_phase(const ek_grid* g, int jac, const double* u, const double* fu,
+                           const double* b, double* const* ybuf, double* const* p, int k,
+                           const double* coef_dev, int chunk_base, int m_begin, int m_end,
+                           double gamma, ek_leja_state* st, double* work,
+                           const double* const* halo_b, const ek_peer* peer,
+                           double* win_local, int64_t epoch0, int phase, void* stream) {
+    if (phase < 1 || phase > 3) {
+        set_error("ek_leja_run_peer_phase: phase must be 1 (pass), 2 (decide) or 3");
+        return EK_ERR_INVALID;
+    }
     if (!grid_ok(g)) return EK_ERR_INVALID;
     if (k < 1 || k > 8 || !peer || !win_local || !halo_b || !g->slab || g->rows < 2 ||
         g->dim < 2) {
@@ -608,11 +629,15 @@ int ek_leja_run_peer(const ek_grid* g, int jac, const double* u, const double* f
         a.hy = (m == 1) ? halo_b[1]
                         : (const double*)((const char*)win_local + EK_PEER_HALO_OFFSET) +
                               (e & 1) * 2 * (int64_t)g->ncomp * rowlen;
-        const int rc = launch_stencil<EP_LEJA>(ev, a, s);
-        if (rc != EK_OK) return rc;
-        k_peer_decide<<<1, 32, 0, s>>>(st, peer, (long)e, coef_dev, m - chunk_base, m, k,
-                                       jac == EK_JAC_FD ? 1 : 0);
-        EK_LAUNCH_CHECK("k_peer_decide");
+        if (phase & 1) {
+            const int rc = launch_stencil<EP_LEJA>(ev, a, s);
+            if (rc != EK_OK) return rc;
+        }
+        if (phase & 2) {
+            k_peer_decide<<<1, 32, 0, s>>>(st, peer, (long)e, coef_dev, m - chunk_base, m, k,
+                                           jac == EK_JAC_FD ? 1 : 0);
+            EK_LAUNCH_CHECK("k_peer_decide");
+        }
     }
     return EK_OK;
 }

@@ -214,6 +214,74 @@ class LejaResult:
     freeze_iters: list
 
 
+_KMAX = 8  # accumulators one fused pass / state block carries
+
+
+def _vertical_wide(J, b, bd, l, coeffs, h, est, tol, xi, max_points):
+    """A vertical group of more than _KMAX coefficients (the reference has
+    no cap, leja.py:144-150): the shared recurrence runs once per iteration
+    (one J.apply_dev, so the counter sees exactly the reference's charges),
+    and the accumulators are updated in blocks of _KMAX, each with its own
+    state block (same ||y_m||, its own freeze decisions); the loop ends when
+    every block has frozen, at the largest freeze point — leja.py:167-189
+    unchanged."""
+    n = bd.numel()
+    k = len(coeffs)
+    c, gamma = est.c, est.gamma
+    blocks = [list(range(i, min(k, i + _KMAX))) for i in range(0, k, _KMAX)]
+    m_avail = min(_CHUNK, max_points)
+    dds = _dd_group(l, [ci * h for ci in coeffs], est, xi, m_avail)
+    ps = [D.empty(n) for _ in range(k)]
+    tabs, sts = [], []
+    ws = D.work_ptr()
+    for blk in blocks:
+        t = _CoefTable(len(blk))
+        t.load(0, m_avail, [dds[i] for i in blk], c, gamma, xi)
+        st = D.DevState(N.LejaState, tol=float(tol), nu=0.0, k=len(blk), p_init=0)
+        N.check(N.lib().ek_leja_begin_len(n, C.c_void_p(bd.data_ptr()),
+                                          N.ptrs([ps[i] for i in blk]), len(blk),
+                                          C.c_void_p(t.dev.data_ptr()), st.ptr, ws, D.stream()),
+                "ek_leja_begin_len")
+        tabs.append(t)
+        sts.append(st)
+    hs = [st.read() for st in sts]
+    done = [bool(hh.done) for hh in hs]
+    ybuf = [D.empty(n), D.empty(n)]
+    m, base = 1, 0
+    while not all(done) and m < max_points:
+        if m >= m_avail:  # next 32-point chunk (leja.py:168-171)
+            m_avail = min(m_avail + _CHUNK, max_points)
+            dds = _dd_group(l, [ci * h for ci in coeffs], est, xi, m_avail)
+            base = m
+            for blk, t in zip(blocks, tabs):
+                t.load(base, m_avail, [dds[i] for i in blk], c, gamma, xi)
+        y = bd if m == 1 else ybuf[(m - 1) & 1]
+        jv = J.apply_dev(y)
+        for bi, (blk, t, st) in enumerate(zip(blocks, tabs, sts)):
+            if done[bi]:
+                continue
+            N.check(N.lib().ek_leja_update(
+                n, C.c_void_p(jv.data_ptr()), C.c_void_p(y.data_ptr()),
+                C.c_void_p(ybuf[m & 1].data_ptr()), N.ptrs([ps[i] for i in blk]), len(blk),
+                C.c_void_p(t.dev.data_ptr()), base, m, float(gamma), 0, st.ptr, ws,
+                D.stream()), "ek_leja_update")
+        for bi, st in enumerate(sts):
+            if not done[bi]:
+                hs[bi] = st.read()
+                if hs[bi].status == N.ST_NORM_NONFINITE:
+                    raise NonConvergence("polynomial iteration diverged", iters=int(hs[bi].iters))
+                done[bi] = bool(hs[bi].done)
+        m += 1
+    if not all(done):
+        stalled = [coeffs[i] for bi, blk in enumerate(blocks) for j, i in enumerate(blk)
+                   if (hs[bi].active >> j) & 1]
+        raise NonConvergence(f"no convergence in {max_points} Leja points",
+                             iters=max_points, detail={"stalled_coefficients": stalled})
+    freeze = [int(hs[bi].freeze[j]) for bi, blk in enumerate(blocks) for j in range(len(blk))]
+    return LejaResult(vectors=[D.like_input(p, b) for p in ps], iters=max(freeze),
+                      freeze_iters=freeze)
+
+
 def leja_interpolate(J: MatrixFreeOperator, b, l, h, est, tol,
                      xi=None, max_points=DEFAULT_NUM_POINTS):
     """p ~ phi_l(h J) b; returns (p, iters) (leja.py:121-130)."""
@@ -315,8 +383,6 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     for ci in coeffs:
         if not 0.0 < ci <= 1.0:
             raise ValueError("coefficients must lie in (0, 1]")
-    if len(coeffs) > 8:
-        raise ValueError("at most 8 coefficients per vertical group")
     if xi is None:
         xi = get_leja_points(max_points)
     k = len(coeffs)
@@ -325,6 +391,8 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     n = bd.numel()
     if n != J.dim:
         raise ValueError(f"expected vector of length {J.dim}, got {n}")
+    if k > _KMAX:
+        return _vertical_wide(J, b, bd, l, coeffs, h, est, tol, xi, max_points)
 
     m_avail = min(_CHUNK, max_points)
     # a group that needed more than one chunk last time (the engines pass its

@@ -1,0 +1,59 @@
+"""API edges of the drop-in (VERDICT r1 "API deviations"): a vertical Leja
+group with more coefficients than one fused pass carries (the reference has
+no cap, leja.py:144-150) gives the reference's results, iterations, freeze
+points and RHS charges (checked against the oracle, which restates the
+reference loop)."""
+
+import numpy as np
+import pytest
+
+import paper_2211_08948_b200 as ek
+from paper_2211_08948_b200 import ext
+from oracle import np_fields as OF, np_integrate as OI, np_phi as OP
+
+pytestmark = pytest.mark.gpu
+
+
+def test_wide_vertical_group_matches_oracle():
+    n = 32
+    xi = ek.get_leja_points(400)
+    p, q = ext.brusselator_periodic_problem(n=n), OF.brusselator_periodic(n=n)
+    rhs = ek.CountingRhs(p.rhs)
+    sys_ = ek.make_linearized(rhs, p.u0)
+    orhs = OP.CountedRhs(q.rhs)
+    osys = OI.linearize(orhs, q.u0)
+    lam, _ = OP.power_iterate(osys.J)
+    est = ek.make_estimate(lam)
+    dt = 20.0 / abs(est.alpha)
+    coeffs = [i / 11.0 for i in range(1, 12)]          # 11 > 8 accumulators
+    b = sys_.f_n * dt
+    c0 = rhs.counter.count
+    res = ek.leja_interpolate_vertical(sys_.J, b, 1, coeffs, dt, est, 1e-10, xi=xi)
+    charges = rhs.counter.count - c0
+    oc0 = orhs.counter.count
+    ores = OP.leja_vertical(osys.J, osys.f_n * dt, 1, coeffs, dt, est, 1e-10, xi)
+    assert res.iters == ores.iters
+    assert res.freeze_iters == ores.freeze_iters
+    assert charges == orhs.counter.count - oc0
+    for g, o in zip(res.vectors, ores.vectors):
+        assert np.linalg.norm(g - o) <= 1e-7 * np.linalg.norm(o)
+    # and each equals the fused single-coefficient call (leja.py:121-130)
+    for ci, g in zip(coeffs[::5], res.vectors[::5]):
+        single, it = ek.leja_interpolate(sys_.J, b, 1, ci * dt, est, 1e-10, xi=xi)
+        assert np.linalg.norm(single - g) <= 1e-7 * np.linalg.norm(g)
+
+
+def test_wide_vertical_group_dense_operator():
+    rng = np.random.default_rng(5)
+    m = 40
+    A = -np.diag(rng.uniform(0.5, 30.0, m)) + 0.01 * rng.standard_normal((m, m))
+    b = rng.standard_normal(m)
+    op = ek.MatrixFreeOperator.from_matrix(A)
+    est = ek.make_estimate(np.linalg.eigvals(A).real.min())
+    coeffs = [0.1 * i for i in range(1, 11)]
+    xi = ek.get_leja_points(400)
+    res = ek.leja_interpolate_vertical(op, b, 2, coeffs, 0.5, est, 1e-12, xi=xi)
+    for ci, v in zip(coeffs, res.vectors):
+        exact = ek.dense_phi_action(2, ci * 0.5 * A, b)
+        assert np.linalg.norm(v - exact) <= 1e-9 * np.linalg.norm(exact)
+    assert res.iters == max(res.freeze_iters)
