@@ -266,13 +266,17 @@ def run_ours(args, rank, world, local):
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None, "traffic": traffic,
-            "kernel": "k_march2d<PBruss<true>, EV_FD, EP_LEJA, K, S> for k >= 3 accumulators "
-                      "(bulk-copy row march), k_tma2d<.., K, 4> (TMA 32x8 chunks) for k <= 2: "
-                      "fused FD Jv + Leja recurrence + k accumulators + ||y||^2 + device "
-                      "freeze test",
+            "kernel": "k_march2d<PBruss<true>, EV_FD, EP_LEJA, K, S> (bulk-copy row march "
+                      "with a producer warp): fused FD Jv + Leja recurrence + k accumulators "
+                      "+ ||y||^2 + device freeze test",
             "bytes_model": "algorithmic, SURVEY.md §8(d) d3: 8*N*(4+2*k_active) per launch "
                            "(reads u, f(u_n), y, p_1..k; writes y', p_1..k), N = 2*n^2",
             "achieved_pass_bytes": kp / kt / 1e9 if kt > 0 else None,
+            "frac_pass_bytes": kp / kt / 1e9 / peak if kt > 0 else None,
+            "frac_note": "frac uses SURVEY's algorithmic bytes, which count a read of f(u_n) "
+                         "that the fused pass replaces by re-evaluating f from the u "
+                         "neighbourhood it reads anyway, so frac can exceed 1; "
+                         "frac_pass_bytes is the fraction on the bytes the pass moves",
             "pass_bytes_model": "8*N*(3+2*k_active): the bytes this kernel moves (f(u_n) is "
                                 "re-evaluated from the u neighbourhood instead of read)",
             "launches": kl, "avg_launch_ms": kt / kl * 1e3 if kl else None,

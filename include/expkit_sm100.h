@@ -163,8 +163,9 @@ int ek_version(void);
 /* Number of kernels this library has launched (process-wide). */
 long long ek_launch_count(void);
 /* Select the stencil staging of 2-D grids: 3 (default) = auto (bulk-copy
- * row march k_march2d for Leja passes with k >= 3 accumulators, TMA 32 x 8
- * chunks k_tma2d otherwise), 2 = row march everywhere, 1 = TMA chunks
+ * row march k_march2d for every Leja pass, TMA 32 x 8 chunks k_tma2d for
+ * the other passes), 4 = round 1's auto (march only while >= 3 Leja
+ * accumulators are active), 2 = row march everywhere, 1 = TMA chunks
  * everywhere, 0 = register-staged; 3-D grids use the TMA plane march for
  * any nonzero mode. A negative mode only queries. Returns the previous
  * setting. All give bit-identical pointwise results (block partial sums of

@@ -264,18 +264,16 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
     static int occ = 0;  // one per template instantiation
     if constexpr (P::DIM == 2) {
         TmaMaps maps;
-        // auto (3): the row march where it measured faster on the B200 (Leja
-        // with k >= 3 ACTIVE accumulators: 0.436 vs 0.498 ms at k = 3, config
-        // 4), 32 x 8 chunks otherwise (k = 2: 0.340 vs 0.392 ms, k = 1: 0.252
-        // vs 0.347 ms). The active count changes on the device as
-        // accumulators freeze, so a K >= 3 Leja iteration is launched as a
-        // pair — march (runs iff >= 3 active) then chunks (runs iff <= 2
-        // active) — and exactly one of them does the pass (the other exits at
-        // its first read of the state block: if the march ran, it advanced
-        // st->m; in slab mode the decision waits for the decide kernel, so
-        // the count the chunk kernel reads is still the one the march saw).
-        const bool pair = g_tma_mode == 3 && EP == EP_LEJA && K >= 3 && march_ok(a);
-        const bool march = g_tma_mode == 2 || pair;
+        // auto (3): the row march for every Leja pass — with its producer
+        // warp it is the faster staging at every accumulator count on the
+        // B200 (config 4: k = 1 0.265 vs 0.274 ms, k = 2 0.318 vs 0.342 ms,
+        // k = 3 0.403 vs 0.499 ms for the 32 x 8 chunks); chunks for the
+        // other passes. (Mode 4 keeps round 1's pairing for A/B runs: march
+        // iff >= 3 accumulators are active, chunks iff <= 2, each launch of a
+        // pair exiting at its first read of the state block unless it is
+        // the one that runs.)
+        const bool pair = g_tma_mode == 4 && EP == EP_LEJA && K >= 3 && march_ok(a);
+        const bool march = g_tma_mode == 2 || pair || (g_tma_mode == 3 && EP == EP_LEJA);
         if (march && march_ok(a)) {
             constexpr int S = tma_stages2<EV, EP, P::NC, K>();
             constexpr int SMEM = S * stage2_doubles<EV, EP, P::NC, K>() * 8;
@@ -283,7 +281,7 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
             auto kern = k_march2d<P, EV, EP, K, S>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, T2, SMEM) !=
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT2, SMEM) !=
                         cudaSuccess || tocc < 1)
                     tocc = 1;
             }
@@ -295,7 +293,7 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
             const unsigned grid = (unsigned)(cap >= ns ? ns * ng : cap);
             KArgs am = a;
             if (pair) { am.act_lo = 3; am.act_hi = 8; }
-            kern<<<grid, T2, SMEM, s>>>(am);
+            kern<<<grid, NT2, SMEM, s>>>(am);
             EK_LAUNCH_CHECK("bulk-copy march stencil launch");
             if (!pair) return EK_OK;
         }

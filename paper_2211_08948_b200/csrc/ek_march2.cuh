@@ -28,8 +28,12 @@
 namespace ek {
 
 constexpr int W2 = 256;    // columns per strip
-constexpr int T2 = 256;    // threads: one column each
+constexpr int T2 = 256;    // compute threads: one column each
 constexpr int NW2 = T2 / 32;
+#ifndef EK_PROD2
+#define EK_PROD2 1  // 1: one extra producer warp issues the row copies
+#endif
+constexpr int NT2 = T2 + (EK_PROD2 ? 32 : 0);  // threads per block
 constexpr int RAW2 = 272;  // doubles per raw row slot: element e <-> column j0 - 2 + e
 constexpr int CTR2 = 256;  // doubles per centre row slot
 
@@ -199,14 +203,18 @@ __host__ __device__ __forceinline__ int march2_segs(long G, int ns) {
 }
 
 template <class P, int EV, int EP, int K, int S>
-__global__ void __launch_bounds__(T2, 2) k_march2d(const KArgs a) {
+__global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
     static_assert(S >= 4, "row ring needs i-1, i, i+1 and one in flight");
     constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
     constexpr int NR = nraw<EV>();
     constexpr int SD = stage2_doubles<EV, EP, NC, K>();
     extern __shared__ __align__(1024) double smem[];
     __shared__ __align__(8) uint64_t full[S];
+#if EK_PROD2
+    __shared__ __align__(8) uint64_t empty[S];  // the NW2 compute warps released stage s
+#else
     __shared__ int released[S];  // warps that released stage s, cumulative
+#endif
 
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
@@ -232,13 +240,19 @@ __global__ void __launch_bounds__(T2, 2) k_march2d(const KArgs a) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
+#if EK_PROD2
+            mbar_init(&empty[s], NW2);
+#else
             released[s] = 0;
+#endif
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#if !EK_PROD2
         if (blockIdx.x < nitems) {
             const Item2 it0 = item2(blockIdx.x, ns, ng, rows);
             for (int s = 0; s < S; ++s) issue_ahead(it0, s - S, s);
         }
+#endif
     }
     __syncthreads();
 
@@ -246,12 +260,40 @@ __global__ void __launch_bounds__(T2, 2) k_march2d(const KArgs a) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
+#if EK_PROD2
+    // Producer warp (the last one): issues every row of this block's items
+    // in sequence order into its ring stage as soon as the NW2 compute warps
+    // have released the stage's previous row (as in k_tma3d).
+    if ((int)(threadIdx.x >> 5) == NW2) {
+        if (lane == 0) {
+            long q = 0;
+            for (long tt = blockIdx.x; tt < nitems; tt += G) {
+                const Item2 it = item2(tt, ns, ng, rows);
+                for (int pos = 0; pos < it.L + 2; ++pos, ++q) {
+                    const int s = (int)(q % S);
+                    if (q >= S) mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
+                    issue_row<EV, EP, NC, K>(a, smem + s * SD, &full[s], it, pos, rows,
+                                             ctr_mask(ctl));
+                }
+            }
+        }
+        __syncwarp();
+        reduce_and_finalize<EV, EP, NQ, NT2>(a, acc);
+        return;
+    }
+#endif
+
     auto wait_full = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
     auto release = [&](int q, const Item2& it, int pos) {
         __syncwarp();
         if (lane == 0) {
             const int s = q % S;
+#if EK_PROD2
+            (void)it; (void)pos;
+            mbar_arrive(&empty[s]);
+#else
             if ((atomicAdd(&released[s], 1) + 1) % NW2 == 0) issue_ahead(it, pos, s);
+#endif
         }
     };
 
@@ -279,7 +321,7 @@ __global__ void __launch_bounds__(T2, 2) k_march2d(const KArgs a) {
         release(q0 + it.L + 1, it, it.L + 1);
         q0 += it.L + 2;
     }
-    reduce_and_finalize<EV, EP, NQ, T2>(a, acc);
+    reduce_and_finalize<EV, EP, NQ, NT2>(a, acc);
 }
 
 }  // namespace ek

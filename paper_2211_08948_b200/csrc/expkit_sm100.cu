@@ -205,7 +205,7 @@ int ek_version(void) { return 1; }
 long long ek_launch_count(void) { return g_launches.load(); }
 int ek_set_tma(int mode) {
     const int old = g_tma_mode;
-    if (mode >= 0) g_tma_mode = mode > 3 ? 3 : mode;
+    if (mode >= 0) g_tma_mode = mode > 4 ? 3 : mode;
     return old;
 }
 
