@@ -171,6 +171,9 @@ long long ek_launch_count(void);
  * setting. All give bit-identical pointwise results (block partial sums of
  * norms / dots are grouped differently). */
 int ek_set_tma(int mode);
+/* Auto mode: the passes (bit 1 << EP, EP_STORE = 0, LEJA, POWER, ARN, REM,
+ * RHSN) staged by the row march; default 1 << 1 (Leja). Negative: query. */
+int ek_set_march(int mask);
 /* Bytes of device workspace (block partials) any call on this grid needs. */
 int64_t ek_workspace_bytes(const ek_grid* g);
 /* Stream-ordered copies (kind: 1 = host->device, 2 = device->host; a copy

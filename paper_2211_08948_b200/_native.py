@@ -87,6 +87,7 @@ _SIGS = {
     "ek_version": (_I, []),
     "ek_launch_count": (C.c_longlong, []),
     "ek_set_tma": (_I, [_I]),
+    "ek_set_march": (_I, [_I]),
     "ek_grid_len": (_L, [C.POINTER(Grid)]),
     "ek_workspace_bytes": (_L, [C.POINTER(Grid)]),
     "ek_copy": (_I, [_P, _P, _L, _I, _P]),
@@ -176,6 +177,8 @@ def lib():
         fn.argtypes = args
     if os.environ.get("EK_TMA_MODE"):  # A/B runs of the stencil staging (tools/)
         handle.ek_set_tma(int(os.environ["EK_TMA_MODE"]))
+    if os.environ.get("EK_MARCH_MASK"):
+        handle.ek_set_march(int(os.environ["EK_MARCH_MASK"]))
     _lib = handle
     return _lib
 

@@ -83,6 +83,7 @@ inline bool march_ok(const KArgs& a) {
 // 2-D staging: 0 register-staged k_stencil2d, 1 TMA 32x8 chunks (k_tma2d),
 // 2 TMA row march (k_march2d, default). 3-D: any nonzero mode = k_tma3d.
 extern int g_tma_mode;
+extern int g_march_mask;  // auto mode: passes (bit EP_*) staged by the row march
 
 // TMA stage count: as deep as fits two resident blocks per SM.
 template <int EV, int EP, int NC, int K>
@@ -273,7 +274,8 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
         // pair exiting at its first read of the state block unless it is
         // the one that runs.)
         const bool pair = g_tma_mode == 4 && EP == EP_LEJA && K >= 3 && march_ok(a);
-        const bool march = g_tma_mode == 2 || pair || (g_tma_mode == 3 && EP == EP_LEJA);
+        const bool march = g_tma_mode == 2 || pair ||
+                           (g_tma_mode == 3 && ((g_march_mask >> EP) & 1));
         if (march && march_ok(a)) {
             constexpr int S = tma_stages2<EV, EP, P::NC, K>();
             constexpr int SMEM = S * stage2_doubles<EV, EP, P::NC, K>() * 8;

@@ -156,13 +156,31 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
 #pragma unroll
     for (int q = 0; q < 8; ++q)
         if (q < a.nk) vec = vec && al16d(a.p[q]);
-    EK_FOR4(e0, a.len) {
+    if (fold) {
+        // read-only pass (||b||^2): 4 groups of 4 elements per thread and
+        // iteration, all 8 loads issued before use (128 B in flight per
+        // thread instead of 32 B: a lone streaming read needs the depth)
+        const int64_t stride = (int64_t)gridDim.x * TPB * 4;
+        for (int64_t e0 = ((int64_t)blockIdx.x * TPB + threadIdx.x) * 4; e0 < a.len;
+             e0 += 4 * stride) {
+            double y[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t e = e0 + u * stride;
+                ld4(a.b, e, a.len, vec && e + 4 <= a.len, y[u]);  // zeros past len
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int w = 0; w < 4; ++w) acc[0] += y[u][w] * y[u][w];
+        }
+    } else EK_FOR4(e0, a.len) {
         const bool full = vec && e0 + 4 <= a.len;
         double y[4];
         ld4(a.b, e0, a.len, full, y);
 #pragma unroll
         for (int w = 0; w < 4; ++w) acc[0] += y[w] * y[w];  // zeros past len
-        if (!fold) {
+        {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
                 if (q < a.nk) {

@@ -33,6 +33,7 @@ int cuda_status(cudaError_t e, const char* where) {
 
 static std::atomic<long long> g_launches{0};
 int g_tma_mode = 3;  // see ek_set_tma
+int g_march_mask = 1 << EP_LEJA;  // see ek_set_march
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ------------------------------------------------------------- 1-D problem
@@ -206,6 +207,12 @@ long long ek_launch_count(void) { return g_launches.load(); }
 int ek_set_tma(int mode) {
     const int old = g_tma_mode;
     if (mode >= 0) g_tma_mode = mode > 4 ? 3 : mode;
+    return old;
+}
+
+int ek_set_march(int mask) {
+    const int old = g_march_mask;
+    if (mask >= 0) g_march_mask = mask;
     return old;
 }
 
