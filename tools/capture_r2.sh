@@ -21,5 +21,7 @@ cap() {  # name, kernel regex, skip, command...
   python tools/sass_summary.py /tmp/${name}_src.csv > $out/r2_${name}_sass.txt 2>&1
 }
 cap march2d_k3 'k_march2d<.*\(int\)1, \(int\)1, \(int\)3' 12 python tools/kernel_bench.py --k 3 --iters 20 --reps 1
-cap lincomb2 'k_lincomb<2' 8 python bench.py --steps 1 --warmup 3 --no-e2e --no-configs --no-cpu-baseline
+cap march2d_k1 'k_march2d<.*\(int\)1, \(int\)1, \(int\)1' 12 python tools/kernel_bench.py --k 1 --iters 20 --reps 1
+cap leja3d_k1 'k_tma3d<.*\(int\)2, \(int\)1, \(int\)1' 12 python tools/kernel_bench.py --problem advdiff3d --n 512 --k 1 --iters 20 --reps 1
+cap lincomb2 'k_lincomb<\(int\)2' 8 python bench.py --steps 1 --warmup 3 --no-e2e --no-configs --no-cpu-baseline
 cap leja_begin 'k_leja_begin' 8 python bench.py --steps 1 --warmup 3 --no-e2e --no-configs --no-cpu-baseline
