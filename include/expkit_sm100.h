@@ -154,7 +154,9 @@ typedef struct ek_arnoldi_state {
     int32_t status;     /* EK_ST_*                                          */
     int32_t fd_evals;   /* FD Jacobian actions performed                    */
     uint32_t ticket;    /* internal (keep 0)                                */
-    int32_t pad_;
+    int32_t defer;      /* slab mode: passes leave local sums in part[] and
+                           ek_arnoldi_slab_decide applies the gathered ones  */
+    double part[6];     /* local window dots / sums of squares (slab mode)   */
 } ek_arnoldi_state;
 
 /* ------------------------------------------------------------ utilities */
@@ -383,6 +385,33 @@ int ek_arnoldi_run(const ek_grid* g, int jac, const double* u,
                    int j_begin, int j_end,
                    double* H, ek_arnoldi_state* st, int p, int iop, int ldh,
                    double dt, double* work, void* stream);
+
+/* Slab-decomposed Arnoldi with device-side decisions (kiops.py:168-194 on
+ * a row slab). Basis rows are the rank's n-part
+ * followed by the p tail values, replicated on every rank. The state block
+ * has defer = 1: every pass leaves its LOCAL sums in st->part (n-part only:
+ * tails are added once, in the decision) and ek_arnoldi_slab_decide applies
+ * the rank-ordered sums of the gathered [nranks][6] part arrays:
+ *   which 3 after ek_arnoldi_slab_init: beta = ||V[0]||;
+ *   which 0 after pass A (phase 0: Jv of V[jj-1] with the halo rows in
+ *           `halo`, augmentation, window dots): H[lo.., jj-1] (+ tail dots),
+ *           non-finite Jacobian action -> status;
+ *   which 1 after pass B (phase 1: CGS subtraction): ||w||, happy test,
+ *           H[jj, jj-1];
+ *   which 2 after pass C (phase 2: V[jj] /= ||w||): ||V[jj,:n]|| (the next
+ *           FD increment).
+ * Every rank takes the same decisions; no host synchronisation between the
+ * passes (the all-gathers are stream-ordered NCCL collectives). */
+int ek_arnoldi_slab_init(int64_t n, int p, const double* src, const double* tail_host,
+                         double* V0, ek_arnoldi_state* st, double* work, void* stream);
+int ek_arnoldi_slab_pass(const ek_grid* g, int jac, const double* u, const double* fu,
+                         double* const* V, const double* const* aug, const int* aug_tail,
+                         int naug, double aug_scale, int jj, int phase, double* H,
+                         ek_arnoldi_state* st, int p, int iop, int ldh, double dt,
+                         double* work, const double* const* halo, void* stream);
+int ek_arnoldi_slab_decide(double* const* V, int64_t n, int p, int jj, int iop, double* H,
+                           int ldh, ek_arnoldi_state* st, const double* gathered, int nranks,
+                           int which, void* stream);
 
 /* Generic-operator Arnoldi: pass A with the (already scaled) action jv. */
 int ek_arnoldi_augment(int64_t n, int p, const double* jv, double* const* V,

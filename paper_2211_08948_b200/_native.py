@@ -73,7 +73,7 @@ class ArnoldiState(C.Structure):
                 ("tol", C.c_double), ("beta", C.c_double), ("j", C.c_int32),
                 ("happy", C.c_int32), ("status", C.c_int32),
                 ("fd_evals", C.c_int32), ("ticket", C.c_uint32),
-                ("pad_", C.c_int32)]
+                ("defer", C.c_int32), ("part", C.c_double * 6)]
 
 
 _P = C.c_void_p
@@ -123,6 +123,10 @@ _SIGS = {
     "ek_leja_run_peer_phase": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
                                     _I, _I, _D, _P, _P, _PP, _P, _P, _L, _I, _P]),
     "ek_arnoldi_init": (_I, [_L, _I, _P, C.POINTER(_D), _P, _P, _P, _P]),
+    "ek_arnoldi_slab_init": (_I, [_L, _I, _P, C.POINTER(_D), _P, _P, _P, _P]),
+    "ek_arnoldi_slab_pass": (_I, [C.POINTER(Grid), _I, _P, _P, _PP, _PP, C.POINTER(_I), _I,
+                                  _D, _I, _I, _P, _P, _I, _I, _I, _D, _P, _PP, _P]),
+    "ek_arnoldi_slab_decide": (_I, [_PP, _L, _I, _I, _I, _P, _I, _P, _P, _I, _I, _P]),
     "ek_arnoldi_run": (_I, [C.POINTER(Grid), _I, _P, _P, _PP, _PP,
                             C.POINTER(_I), _I, _D, _I, _I, _P, _P, _I, _I, _I,
                             _D, _P, _P]),

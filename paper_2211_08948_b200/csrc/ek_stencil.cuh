@@ -883,6 +883,16 @@ __device__ void finalize(const KArgs& a, const double* tot) {
     } else if constexpr (EP == EP_ARN) {
         ek_arnoldi_state* st = (ek_arnoldi_state*)a.st;
         if (EV == EV_FD && st->nvn != 0.0) st->fd_evals += 1;
+        if (st->defer) {  // slab mode: local sums; ek_arnoldi_slab_decide finishes
+            for (int q = 0; q < 5; ++q) st->part[q] = tot[q];
+            const long n = a.g.ncomp * a.npts;
+            const int p = (int)a.n_aug;
+            const double* prev = a.win[a.nwin - 1];
+            double* cur = a.out;
+            for (int t = 0; t + 1 < p; ++t) cur[n + t] = prev[n + t + 1];
+            if (p > 0) cur[n + p - 1] = 0.0;
+            return;
+        }
         if (EV == EV_FD && tot[4] > 0.0) {
             st->status = EK_ST_JV_NONFINITE;
             return;

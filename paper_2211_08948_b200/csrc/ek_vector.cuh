@@ -432,6 +432,14 @@ __global__ void __launch_bounds__(TPB) k_arn_init(const ArnVArgs a) {
         gather_partials<1>(a.work, gridDim.x, tot);
         if (threadIdx.x == 0) {
             double ssq = tot[0];
+            if (a.st->defer) {  // slab: beta from the gathered sums (which 3)
+                for (int t = 0; t < a.p; ++t) a.w[a.n + t] = a.tail0[t];
+                a.st->part[0] = tot[0];
+                a.st->happy = 0;
+                a.st->status = EK_ST_OK;
+                a.st->j = 0;
+                return;
+            }
             for (int t = 0; t < a.p; ++t) {
                 a.w[a.n + t] = a.tail0[t];
                 ssq += a.tail0[t] * a.tail0[t];
@@ -497,6 +505,7 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) h[q] = q < a.nwin ? a.H[(long)(lo + q) * a.ldh + (a.jj - 1)] : 0.0;
     const int64_t len = a.n + a.p;
+    const bool nonly = cst->defer != 0;  // slab: the tail is added once, in the decision
     double acc[1] = {0.0};
     bool vec = al16d(a.w);
 #pragma unroll
@@ -520,7 +529,7 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             wv[w] = wv[w] - t[w];
-            acc[0] += wv[w] * wv[w];  // zeros past len
+            if (!nonly || e0 + w < a.n) acc[0] += wv[w] * wv[w];  // zeros past len
         }
         st4(a.w, e0, len, full, wv);
     }
@@ -530,6 +539,10 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
         gather_partials<1>(a.work, gridDim.x, tot);
         if (threadIdx.x == 0) {
             ek_arnoldi_state* st = a.st;
+            if (st->defer) {
+                st->part[0] = tot[0];
+                return;
+            }
             const double nrm = sqrt(tot[0]);
             st->nrm = nrm;
             if (nrm < st->tol) {  // happy breakdown, kiops.py:190-192
@@ -566,9 +579,57 @@ __global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
         double tot[1];
         gather_partials<1>(a.work, gridDim.x, tot);
         if (threadIdx.x == 0) {
-            a.st->nvn = sqrt(tot[0]);
+            if (a.st->defer) a.st->part[0] = tot[0];
+            else a.st->nvn = sqrt(tot[0]);
             a.st->j = a.jj;
         }
+    }
+}
+
+// Slab mode: the decision of one Arnoldi pass from the gathered per-rank
+// part[6] arrays (rank order; tails, replicated on every rank, added once).
+__global__ void k_arn_decide(const ArnVArgs a, const double* g, int nranks, int which) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    ek_arnoldi_state* st = a.st;
+    auto sum = [&](int q) {
+        double s = g[q];
+        for (int r = 1; r < nranks; ++r) s = s + g[6 * r + q];
+        return s;
+    };
+    const int64_t n = a.n;
+    if (which == 3) {  // after init: beta = ||[w ; tail]||  (kiops.py:176)
+        double ssq = sum(0);
+        for (int t = 0; t < a.p; ++t) ssq += a.w[n + t] * a.w[n + t];
+        st->nrm = sqrt(ssq);
+        st->beta = st->nrm;
+        return;
+    }
+    if (st->happy || st->status) return;
+    if (which == 0) {  // after pass A: H column (kiops.py:187) + non-finite Jv
+        if (sum(4) > 0.0) {
+            st->status = EK_ST_JV_NONFINITE;
+            return;
+        }
+        const int lo = a.jj - a.nwin;
+        for (int q = 0; q < a.nwin; ++q) {
+            double tl = 0.0;
+            for (int t = 0; t < a.p; ++t) tl += a.win[q][n + t] * a.w[n + t];
+            a.H[(long)(lo + q) * a.ldh + (a.jj - 1)] = sum(q) + tl;
+        }
+        a.H[(long)a.jj * a.ldh + (a.jj - 1)] = 0.0;
+    } else if (which == 1) {  // after pass B: ||w||, happy breakdown (kiops.py:188-193)
+        double ssq = sum(0);
+        for (int t = 0; t < a.p; ++t) ssq += a.w[n + t] * a.w[n + t];
+        const double nrm = sqrt(ssq);
+        st->nrm = nrm;
+        if (nrm < st->tol) {
+            st->happy = 1;
+            st->j = a.jj;
+        } else {
+            a.H[(long)a.jj * a.ldh + (a.jj - 1)] = nrm;
+        }
+    } else {  // after pass C: ||V[jj,:n]|| for the next FD increment
+        st->nvn = sqrt(sum(0));
     }
 }
 

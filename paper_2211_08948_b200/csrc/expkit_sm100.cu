@@ -719,6 +719,82 @@ int ek_arnoldi_run(const ek_grid* g, int jac, const double* u, const double* fu,
     return EK_OK;
 }
 
+int ek_arnoldi_slab_init(int64_t n, int p, const double* src, const double* tail_host,
+                         double* V0, ek_arnoldi_state* st, double* work, void* stream) {
+    if (p < 0 || p > 5) {
+        set_error("ek_arnoldi_slab_init: p=%d out of range", p);
+        return EK_ERR_INVALID;
+    }
+    ArnVArgs a{};
+    a.n = n; a.p = p; a.src = src; a.w = V0; a.st = st; a.work = work;
+    for (int t = 0; t < p; ++t) a.tail0[t] = tail_host[t];
+    k_arn_init<<<vgrid4(n), TPB, 0, (cudaStream_t)stream>>>(a);
+    EK_LAUNCH_CHECK("k_arn_init");
+    return EK_OK;
+}
+
+int ek_arnoldi_slab_pass(const ek_grid* g, int jac, const double* u, const double* fu,
+                         double* const* V, const double* const* aug, const int* aug_tail,
+                         int naug, double aug_scale, int jj, int phase, double* H,
+                         ek_arnoldi_state* st, int p, int iop, int ldh, double dt,
+                         double* work, const double* const* halo, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (iop < 1 || iop > 4 || p < 1 || p > 5 || naug > 5 || iop + naug > 8 || phase < 0 ||
+        phase > 2 || jj < 0 || (phase < 2 && jj < 1)) {
+        set_error("ek_arnoldi_slab_pass: iop=%d p=%d naug=%d phase=%d jj=%d out of range", iop,
+                  p, naug, phase, jj);
+        return EK_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = ek_grid_len(g);
+    ArnVArgs b{};
+    b.n = n; b.p = p; b.H = H; b.ldh = ldh; b.st = st; b.work = work; b.jj = jj;
+    if (jj > 0) arn_window(b, V, jj, iop);
+    b.w = V[jj];
+    if (phase == 0) {
+        const int ev = jv_ev(g, jac);
+        if (ev < 0) return EK_ERR_UNSUPPORTED;
+        KArgs a;
+        base_args(a, g, halo);
+        a.u = u; a.fu = fu; a.st = st; a.work = work; a.H = H; a.ldh = ldh; a.dt = dt;
+        a.n_aug = p; a.naug = naug; a.aug_scale = aug_scale;
+        for (int t = 0; t < naug; ++t) {
+            a.aug[t] = aug[t];
+            a.aug_tail[t] = aug_tail[t];
+        }
+        a.nwin = b.nwin;
+        for (int q = 0; q < 4; ++q) a.win[q] = b.win[q];
+        a.jj = jj;
+        a.y = V[jj - 1];
+        a.out = V[jj];
+        return launch_stencil<EP_ARN>(ev, a, s);
+    }
+    if (phase == 1) {
+        k_arn_orth<<<vgrid4(n + p), TPB, 0, s>>>(b);
+        EK_LAUNCH_CHECK("k_arn_orth");
+    } else {
+        k_arn_scale<<<vgrid4(n + p), TPB, 0, s>>>(b);
+        EK_LAUNCH_CHECK("k_arn_scale");
+    }
+    return EK_OK;
+}
+
+int ek_arnoldi_slab_decide(double* const* V, int64_t n, int p, int jj, int iop, double* H,
+                           int ldh, ek_arnoldi_state* st, const double* gathered, int nranks,
+                           int which, void* stream) {
+    if (which < 0 || which > 3 || nranks < 1 || p < 0 || p > 5) {
+        set_error("ek_arnoldi_slab_decide: which=%d nranks=%d p=%d", which, nranks, p);
+        return EK_ERR_INVALID;
+    }
+    ArnVArgs b{};
+    b.n = n; b.p = p; b.H = H; b.ldh = ldh; b.st = st; b.jj = jj;
+    if (jj > 0) arn_window(b, V, jj, iop);
+    b.w = V[jj];
+    k_arn_decide<<<1, 32, 0, (cudaStream_t)stream>>>(b, gathered, nranks, which);
+    EK_LAUNCH_CHECK("k_arn_decide");
+    return EK_OK;
+}
+
 int ek_arnoldi_augment(int64_t n, int p, const double* jv, double* const* V, int jj, int iop,
                        const double* const* aug, const int* aug_tail, int naug, double aug_scale,
                        double* H, int ldh,

@@ -159,6 +159,21 @@ class SlabComm:
         dist.all_gather_into_tensor(out, part.contiguous(), group=self.group)
         return out.reshape(self.world, 2)
 
+    def allgather_vals(self, part):
+        """[world * k] device tensor of every rank's k-double device view
+        (rank-major), stream-ordered over NCCL (no host sync); host-staged
+        over gloo."""
+        k = part.numel()
+        if self.world == 1:
+            return part.reshape(-1)
+        if self.host_staged:
+            bufs = [torch.empty(k, dtype=torch.float64) for _ in range(self.world)]
+            dist.all_gather(bufs, part.cpu(), group=self.group)
+            return torch.cat(bufs).to(part.device)
+        out = torch.empty(self.world * k, dtype=torch.float64, device=part.device)
+        dist.all_gather_into_tensor(out, part.contiguous(), group=self.group)
+        return out
+
     def allsum(self, values):
         """Rank-ordered sums of a list of host floats (identical on all ranks)."""
         if self.world == 1:
