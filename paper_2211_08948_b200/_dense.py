@@ -101,7 +101,7 @@ def phi_divided_differences_many(l, hs, c, gamma, xi, m):
     `dense_phi_action` (tiny norm: Taylor series; non-finite entries: the
     error path) are computed one by one as before."""
     hs = [float(h) for h in hs]
-    if _matrix_exponential is None or len(hs) < 2 or l < 0:
+    if _matrix_exponential is None or not hs or l < 0:
         return [phi_divided_differences(l, h, c, gamma, xi, m) for h in hs]
     x = np.asarray(xi[:m], dtype=np.float64)
     r = np.arange(m - 1)

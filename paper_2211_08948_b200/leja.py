@@ -173,7 +173,7 @@ def _dd_group(l, hs, est, xi, m_max):
     m = min(m_max, len(xi))
     keys = [_dd_key(l, h, est, xi, m_max) for h in hs]
     miss = [i for i, k in enumerate(keys) if k not in _DD_CACHE]
-    if len(miss) > 1 and m <= _CHUNK and 0 <= l <= 4 and min(hs) >= 0:
+    if miss and m <= _CHUNK and 0 <= l <= 4 and min(hs) >= 0:
         ds = phi_divided_differences_many(l, [hs[i] for i in miss], est.c, est.gamma, xi, m)
         for i, d in zip(miss, ds):
             if not np.isfinite(d).all():  # as divided_differences()

@@ -222,12 +222,12 @@ def test_batched_divided_differences_bit_identical():
                                                phi_divided_differences_many)
     xi = ek.get_leja_points(400)
     rng = np.random.default_rng(3)
-    for _ in range(120):
+    for _ in range(200):
         c = -rng.uniform(1.0, 1e6)
         g = abs(c) / 2.0
         dt = 10.0 ** rng.uniform(-12, -1)
         l = int(rng.integers(0, 5))
         m = int(rng.choice([4, 16, 32]))
-        hs = [ci * dt for ci in sorted(rng.uniform(0.05, 1.0, int(rng.integers(2, 4))))]
+        hs = [ci * dt for ci in sorted(rng.uniform(0.05, 1.0, int(rng.integers(1, 4))))]
         for h, d in zip(hs, phi_divided_differences_many(l, hs, c, g, xi, m)):
             assert np.array_equal(d, phi_divided_differences(l, h, c, g, xi, m))
