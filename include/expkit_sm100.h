@@ -117,7 +117,8 @@ typedef struct ek_leja_state {
 /* Scalar reduction slot (norms, dots, flags), device memory. */
 typedef struct ek_scalar_state {
     double val[8];      /* reduced values                                   */
-    int32_t flag;       /* bit0: any nonzero, bit1: any non-finite          */
+    int32_t flag;       /* bit0: any nonzero, bit1: any non-finite, bit2:
+                           non-finite FD Jacobian action (FD remainder)    */
     uint32_t ticket;    /* internal (keep 0)                                */
     int32_t count;
     int32_t status;     /* EK_ST_*                                          */

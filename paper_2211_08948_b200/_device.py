@@ -247,8 +247,9 @@ def global_norm(h):
     """(||x||, flags) from a reduced ek_scalar_state, global in slab mode."""
     if COMM is None:
         return float(h.val[1]), int(h.flag)
-    s, nz, nf = COMM.allsum([float(h.val[0]), float(h.flag & 1), float((h.flag >> 1) & 1)])
-    return math.sqrt(s), (1 if nz > 0 else 0) | (2 if nf > 0 else 0)
+    s, nz, nf, nj = COMM.allsum([float(h.val[0]), float(h.flag & 1), float((h.flag >> 1) & 1),
+                                 float((h.flag >> 2) & 1)])
+    return math.sqrt(s), (1 if nz > 0 else 0) | (2 if nf > 0 else 0) | (4 if nj > 0 else 0)
 
 
 def global_sum(v):

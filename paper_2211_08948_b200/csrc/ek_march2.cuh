@@ -192,7 +192,7 @@ __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, con
         if constexpr (EP == EP_REM && K > 0) z.p[0][c] = ctr[(FU * NC + c) * CTR2 + t];
     }
     double val[NC];
-    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
+    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val, z.jbad);
     epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, z, acc);
 }
 
@@ -205,7 +205,7 @@ __host__ __device__ __forceinline__ int march2_segs(long G, int ns) {
 template <class P, int EV, int EP, int K, int S>
 __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
     static_assert(S >= 4, "row ring needs i-1, i, i+1 and one in flight");
-    constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
     constexpr int NR = nraw<EV>();
     constexpr int SD = stage2_doubles<EV, EP, NC, K>();
     extern __shared__ __align__(1024) double smem[];

@@ -62,6 +62,13 @@ __host__ __device__ constexpr int ep_nq(int ep) {
     return ep == EP_LEJA ? 2 : ep == EP_POWER ? 2 : ep == EP_ARN ? 5 : ep == EP_REM ? 1
          : ep == EP_RHSN ? 3 : 0;
 }
+// accumulators of a pass; the FD remainder also counts non-finite FD
+// Jacobian actions (the reference raises 'non-finite Jacobian action' from
+// fd_jacobian_apply before the remainder check, linalg.py:127-128)
+template <int EV, int EP>
+__host__ __device__ constexpr int nq_of() {
+    return (EP == EP_REM && EV == EV_REMFD) ? 2 : (ep_nq(EP) > 0 ? ep_nq(EP) : 1);
+}
 
 struct Nb {
     double c, xm, xp, ym, yp, zm, zp;  // centre, axis0 -/+, axis1 -/+, axis2 -/+
@@ -350,7 +357,8 @@ __device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const do
 template <class P, int EV, int NCH>
 __device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
                                          const Nb (&nb)[P::NC][NCH],
-                                         const double (&fuc)[P::NC], double (&val)[P::NC]) {
+                                         const double (&fuc)[P::NC], double (&val)[P::NC],
+                                         double& jbad) {
     constexpr int NC = P::NC;
     if constexpr (EV == EV_RHS || EV == EV_LIN) {
         Nb s[NC];
@@ -377,9 +385,13 @@ __device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
         P::f(s0, fk, a.pc);
         P::f(s1, fw, a.pc);
         P::f(s2, fu, a.pc);  // f(u_n)
+        jbad = 0.0;
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
-            val[c] = (fk[c] - fu[c]) - dv(fw[c] - fu[c], ctl.eps_d);  // integrators.py:106
+        for (int c = 0; c < NC; ++c) {
+            const double jd = dv(fw[c] - fu[c], ctl.eps_d);  // J(u_n)(k - u_n), linalg.py:126
+            jbad += isfinite(jd) ? 0.0 : 1.0;
+            val[c] = (fk[c] - fu[c]) - jd;  // integrators.py:106
+        }
     } else if constexpr (EV == EV_REMLIN) {
         Nb s0[NC], s1[NC];
 #pragma unroll
@@ -523,6 +535,7 @@ struct Centre {
     double fu[NC];
     double y[NC];
     double p[K > 0 ? K : 1][NC];
+    double jbad;  // EV_REMFD: non-finite FD Jacobian actions at this point
 };
 
 template <int EV, int EP, int NC, int K>
@@ -625,6 +638,7 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
                 }
             }
             acc[0] += isfinite(r) ? 0.0 : 1.0;
+            if constexpr (EV == EV_REMFD) acc[1] += ctl.y_zero ? 0.0 : z.jbad;
         }
     }
 }
@@ -660,7 +674,7 @@ __device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc
 
 template <class P, int EV, int EP, int RPT, int K>
 __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
-    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = nq_of<EV, EP>();
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -735,7 +749,7 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
             }
             if (i < rows && j < cols) {
                 double val[NC];
-                evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val);
+                evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val, zc[r - 1].jbad);
                 epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, zc[r - 1], acc);
             }
         }
@@ -748,7 +762,7 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
 
 template <class P, int EV, int EP, int RPT, int K>
 __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
-    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NC = P::NC, NCH = ev_nch(EV), NQ = nq_of<EV, EP>();
     Ctl ctl;
     if (!load_ctl<EV, EP>(a, ctl)) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -827,7 +841,7 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
             }
             if (i < rows && kx < n && jy < n) {
                 double val[NC];
-                evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val);
+                evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val, zc[r - 1].jbad);
                 epilogue<EV, EP, NC, K>(a, ctl, i * plane + jy * n + kx, val, zc[r - 1], acc);
             }
         }
@@ -917,6 +931,12 @@ __device__ void finalize(const KArgs& a, const double* tot) {
         if (tot[0] > 0.0) {
             st->flag |= 2;
             st->status = EK_ST_REM_NONFINITE;
+        }
+        if constexpr (EV == EV_REMFD) {
+            if (tot[1] > 0.0) {  // checked first by the host, as fd_jacobian_apply raises first
+                st->flag |= 4;
+                st->status = EK_ST_JV_NONFINITE;
+            }
         }
     }
 }

@@ -246,7 +246,7 @@ __device__ __forceinline__ void tma_point(const KArgs& a, const Ctl& ctl, const 
         if constexpr (EP == EP_REM && K > 0) z.p[0][c] = ctr[(FU * NC + c) * CTR_SLOT + co];
     }
     double val[NC];
-    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
+    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val, z.jbad);
     epilogue<EV, EP, NC, K>(a, ctl, (long)i * cols + j, val, z, acc);
 }
 
@@ -273,7 +273,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // synchronise with each other, only with the copies they consume.
 template <class P, int EV, int EP, int K, int S>
 __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_constant__ TmaMaps maps) {
-    constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
     constexpr int NR = nraw<EV>();
     constexpr int SD = stage_doubles<EV, EP, NC, K>();
     extern __shared__ __align__(1024) double smem[];

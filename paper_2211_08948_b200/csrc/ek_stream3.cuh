@@ -244,7 +244,7 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
         if constexpr (EP == EP_REM && K > 0) z.p[0][c] = ctr[(FU * NC + c) * CTR3 + co];
     }
     double val[NC];
-    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val);
+    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val, z.jbad);
     epilogue<EV, EP, NC, K>(a, ctl, off, val, z, acc);
 }
 
@@ -252,7 +252,7 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
 template <class P, int EV, int EP, int K, int S>
 __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
     static_assert(S >= 4, "plane ring needs i-1, i, i+1 and one in flight");
-    constexpr int NC = P::NC, NQ = ep_nq(EP) > 0 ? ep_nq(EP) : 1;
+    constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
     constexpr int NR = nraw<EV>();
     constexpr int SD = stage3_doubles<EV, EP, NC, K>();
     constexpr int IY = iy3<EV, EP, NC, K>(), PPT = IY * I3X / T3;

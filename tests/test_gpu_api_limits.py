@@ -57,3 +57,27 @@ def test_wide_vertical_group_dense_operator():
         exact = ek.dense_phi_action(2, ci * 0.5 * A, b)
         assert np.linalg.norm(v - exact) <= 1e-9 * np.linalg.norm(exact)
     assert res.iters == max(res.freeze_iters)
+
+
+def test_remainder_nonfinite_messages_match_oracle():
+    """Non-finite stage vectors: the reference's remainder() raises
+    FloatingPointError('non-finite Jacobian action') from
+    fd_jacobian_apply before its own 'non-finite nonlinear remainder'
+    check (linalg.py:127-128, integrators.py:104-108). The fused FD
+    remainder pass flags a non-finite Jacobian action separately (flag bit
+    2, checked first), so the drop-in raises the oracle's message in each
+    case: a NaN, and an entry whose square overflows ||dk|| (eps = 0)."""
+    n = 32
+    p = ext.brusselator_periodic_problem(n=n)
+    q = OF.brusselator_periodic(n=n)
+    sys_ = ek.make_linearized(ek.CountingRhs(p.rhs), p.u0)
+    osys = OI.linearize(OP.CountedRhs(q.rhs), q.u0)
+    for i, val in ((7, np.nan), (7, 1e200), (n * n + 3, -np.inf)):
+        k = p.u0.copy()
+        k[i] = val
+        with np.errstate(all="ignore"):
+            with pytest.raises(FloatingPointError) as oexc:
+                OI.nonlinear_remainder(osys, k)
+        with pytest.raises(FloatingPointError) as exc:
+            ek.remainder(sys_, k)
+        assert str(exc.value) == str(oexc.value), (val, str(exc.value), str(oexc.value))
