@@ -82,6 +82,35 @@ typedef struct ek_grid {
 /* Length of one state vector (ncomp * points, +1 for the semilinear time). */
 int64_t ek_grid_len(const ek_grid* g);
 
+/* ------------------------------------------------- reproducible sums */
+/* norms (and with them every decision and every FD
+ * increment) that are bitwise identical for P = 1/2/4/8 slabs. In repro
+ * mode (ek_set_repro(1); slab decompositions switch it on) the sum channel
+ * of every reducing pass on the Leja / power-iteration / integrator-norm
+ * path is accumulated in integers, independent of the order of the terms
+ * (csrc/ek_xsum.cuh): a local sum is EK_XSLOTS 8-byte integer slots (four
+ * 32-bit-bin sums and the index of the highest bin), merged exactly across
+ * blocks, kernels and ranks and rounded to fp64 once. Whole-grid runs in
+ * repro mode give the same bits as any slab decomposition. Replaces the
+ * reference's np.linalg.norm (leja.py:173, spectrum.py:58, linalg.py:122,
+ * timestep.py:46-52), which has no decomposition to be invariant to. */
+#define EK_XSLOTS 5
+/* part[] of the control blocks (slab mode), red[][] of the peer windows:
+ * slots 0..4 the sum channel (slot 0 an fp64 value, or in repro mode the
+ * EK_XSLOTS integers), slot 5 the non-finite count, slot 6 the format tag
+ * (1.0 = integers). */
+#define EK_PART_SLOTS 8
+#define EK_PART_COUNT 5
+#define EK_PART_TAG 6
+/* Returns the previous setting; negative only queries. */
+int ek_set_repro(int on);
+/* The fp64 value of a merged accumulator: `slots` = [n][EK_XSLOTS] integer
+ * slots (host memory) of n local sums. */
+double ek_xsum_value(const int64_t* slots, int n);
+/* Host-side accumulation of n fp64 terms (sq = 1: their squares) into
+ * slots_out[EK_XSLOTS]: the restatement the tests check the kernels with. */
+void ek_xsum_host(const double* x, int64_t n, int sq, int64_t* slots_out);
+
 /* -------------------------------------------------------- device states */
 /* Leja iteration control block, lives in device memory (leja.py:159-184).
  * The host initialises tol, nu, k (and zeroes the rest) before
@@ -107,7 +136,8 @@ typedef struct ek_leja_state {
                            iteration (see ek_leja_begin_len). Device: 1 when
                            p_i holds d_i[0] b, 0 while the first fused
                            iteration (m = 1) still has to write it       */
-    double part[2];     /* local ||y||^2 and non-finite count                */
+    double part[8];     /* EK_PART_SLOTS: local ||y||^2 and non-finite count
+                           (layout: EK_PART_*)                               */
     int32_t lazy0;      /* host: 1 = if everything freezes at m = 0, do not
                            write p_i = d_i[0] b (the caller uses d_i[0]*b as
                            an expression, ek_lincomb mode 3)                 */
@@ -122,6 +152,11 @@ typedef struct ek_scalar_state {
     uint32_t ticket;    /* internal (keep 0)                                */
     int32_t count;
     int32_t status;     /* EK_ST_*                                          */
+    int64_t xs[5];      /* EK_XSLOTS; repro mode: the integer accumulator of
+                           val[0] (a sum of squares), merged exactly across
+                           ranks                                             */
+    int32_t repro;      /* 1: xs is valid                                   */
+    int32_t pad_;
 } ek_scalar_state;
 
 /* Power iteration control block (spectrum.py:43-63). Host initialises
@@ -140,7 +175,7 @@ typedef struct ek_power_state {
     uint32_t ticket;    /* internal (keep 0)                                */
     int32_t status;     /* EK_ST_*                                          */
     int32_t defer;      /* slab mode, see ek_leja_state                     */
-    double part[2];     /* local sums of the last pass                      */
+    double part[8];     /* EK_PART_SLOTS: local sums of the last pass        */
 } ek_power_state;
 
 /* KIOPS Arnoldi control block (kiops.py:168-194). Host initialises nu, tol. */
@@ -301,9 +336,11 @@ int ek_power_norm(int64_t len, const double* x, int scaled, ek_power_state* st,
 
 /* ----------------------------------------------- slab (multi-GPU) mode */
 /* With state->defer = 1 the reducing kernels leave their local sums in
- * state->part[2]; the caller all-gathers the part[] pairs of every rank
- * (`gathered` = nranks x 2 doubles, device) and applies the decision with
- * the rank-ordered global sums: */
+ * state->part[EK_PART_SLOTS]; the caller all-gathers the part[] blocks of
+ * every rank (`gathered` = nranks x EK_PART_SLOTS slots, device) and applies
+ * the decision with the global sums: the exact merge of the ranks' integer
+ * accumulators in repro mode (identical for every P), else the rank-ordered
+ * fp64 sums: */
 int ek_leja_decide(ek_leja_state* st, const double* gathered, int nranks,
                    const double* coef_dev, int chunk_base, int m, int k, int fd,
                    int begin, void* stream);
@@ -315,7 +352,7 @@ int ek_power_decide(ek_power_state* st, const double* gathered, int nranks,
 /* Fused compute + exchange for the Leja recurrence: every
  * rank owns one device "window" that all ranks map (CUDA IPC):
  *   uint64 flag[8]            flag[r] = e+1 once rank r finished pass e
- *   double red[2][8][2]       [e & 1][r]: rank r's (||y||^2, non-finite) of pass e
+ *   double red[2][8][EK_PART_SLOTS]  [e & 1][r]: rank r's local sums of pass e (EK_PART_*)
  *   double halo[2][2][ncomp][rowlen]  [parity][0: row -1, 1: row `rows`]
  * The fused Leja kernel of pass e stores its boundary rows of y' straight
  * into the neighbours' halo[(e+1) & 1] (reflect ghosts into its own), and
@@ -333,7 +370,7 @@ typedef struct ek_peer {
     int32_t pad_;
     double* win[8];     /* every rank's window as mapped in this process   */
 } ek_peer;
-#define EK_PEER_HALO_OFFSET 512  /* bytes: flags (64) + red (256), aligned */
+#define EK_PEER_HALO_OFFSET 2048 /* bytes: flags (64) + red[2][8][EK_PART_SLOTS] (1024), aligned */
 /* Window size for a slab grid. */
 int64_t ek_peer_window_bytes(const ek_grid* g);
 /* Device allocation (zeroed) plus its CUDA IPC handle (64 bytes out). */
@@ -464,6 +501,12 @@ int ek_l1(int64_t len, const double* x, ek_scalar_state* st, int slot,
  * correction quotient, exact[i] = x[i]/d[i] by the division instruction. */
 int ek_selftest_div(int64_t n, const double* x, const double* d, double* fast,
                     double* exact, void* stream);
+/* Self test of the order-independent sums: sum of x[0..n) (sq = 1: of the
+ * squares) by a grid of `blocks` blocks through the kernels' reduction path;
+ * out_slots[EK_XSLOTS] (device) = the merged accumulator, st->val[0] = its
+ * fp64 value. Synchronises the stream. */
+int ek_selftest_xsum(int64_t n, const double* x, int sq, int blocks, ek_scalar_state* st,
+                     int64_t* out_slots, void* stream);
 /* y = A x, A dense row-major (linalg.py:87-90 from_matrix). */
 int ek_dense_gemv(int64_t n, const double* A, const double* x, double* y,
                   void* stream);

@@ -244,12 +244,33 @@ COMM = None
 
 
 def global_norm(h):
-    """(||x||, flags) from a reduced ek_scalar_state, global in slab mode."""
+    """(||x||, flags) from a reduced ek_scalar_state, global in slab mode:
+    the exact merge of the ranks' integer accumulators in repro mode
+    (identical for every decomposition), else the
+    rank-ordered fp64 sum."""
     if COMM is None:
         return float(h.val[1]), int(h.flag)
-    s, nz, nf, nj = COMM.allsum([float(h.val[0]), float(h.flag & 1), float((h.flag >> 1) & 1),
-                                 float((h.flag >> 2) & 1)])
+    flags = [int(h.flag & 1), int((h.flag >> 1) & 1), int((h.flag >> 2) & 1)]
+    if h.repro:
+        rows = COMM.allgather_ints([int(v) for v in h.xs] + flags)
+        slots = (C.c_int64 * (N.XSLOTS * len(rows)))()
+        for r, row in enumerate(rows):
+            for i in range(N.XSLOTS):
+                slots[r * N.XSLOTS + i] = row[i]
+        s = N.lib().ek_xsum_value(slots, len(rows))
+        nz, nf, nj = (sum(row[N.XSLOTS + i] for row in rows) for i in range(3))
+    else:
+        s, nz, nf, nj = COMM.allsum([float(h.val[0])] + [float(f) for f in flags])
     return math.sqrt(s), (1 if nz > 0 else 0) | (2 if nf > 0 else 0) | (4 if nj > 0 else 0)
+
+
+def set_reproducible(on=True):
+    """Order-independent sums on the Leja / power-iteration / integrator-norm
+    path (csrc/ek_xsum.cuh): norms, and with them every decision and FD
+    increment, are bitwise identical for whole-grid runs and for any slab
+    decomposition. Slab decompositions switch it on (`slab.distribute`).
+    Returns the previous setting."""
+    return bool(N.lib().ek_set_repro(1 if on else 0))
 
 
 def global_sum(v):

@@ -39,7 +39,7 @@ class LejaState(C.Structure):
                 ("status", C.c_int32), ("k", C.c_int32), ("active", C.c_uint32),
                 ("fd_evals", C.c_int32), ("ticket", C.c_uint32),
                 ("iters", C.c_int32), ("freeze", C.c_int32 * 8), ("defer", C.c_int32),
-                ("p_init", C.c_int32), ("part", C.c_double * 2), ("lazy0", C.c_int32),
+                ("p_init", C.c_int32), ("part", C.c_double * 8), ("lazy0", C.c_int32),
                 ("pad_", C.c_int32)]
 
 
@@ -50,13 +50,15 @@ class Peer(C.Structure):
                 ("pad_", C.c_int32), ("win", C.c_void_p * 8)]
 
 
-PEER_HALO_OFFSET = 512
+PEER_HALO_OFFSET = 2048
+XSLOTS, PART_SLOTS, PART_COUNT, PART_TAG = 5, 8, 5, 6
 
 
 class ScalarState(C.Structure):
     _fields_ = [("val", C.c_double * 8), ("flag", C.c_int32),
                 ("ticket", C.c_uint32), ("count", C.c_int32),
-                ("status", C.c_int32)]
+                ("status", C.c_int32), ("xs", C.c_int64 * 5), ("repro", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class PowerState(C.Structure):
@@ -65,7 +67,7 @@ class PowerState(C.Structure):
                 ("max_it", C.c_int32), ("done", C.c_int32),
                 ("converged", C.c_int32), ("fd_evals", C.c_int32),
                 ("ticket", C.c_uint32), ("status", C.c_int32),
-                ("defer", C.c_int32), ("part", C.c_double * 2)]
+                ("defer", C.c_int32), ("part", C.c_double * 8)]
 
 
 class ArnoldiState(C.Structure):
@@ -88,6 +90,10 @@ _SIGS = {
     "ek_launch_count": (C.c_longlong, []),
     "ek_set_tma": (_I, [_I]),
     "ek_set_march": (_I, [_I]),
+    "ek_set_repro": (_I, [_I]),
+    "ek_xsum_value": (_D, [C.POINTER(C.c_int64), _I]),
+    "ek_xsum_host": (None, [_P, _L, _I, C.POINTER(C.c_int64)]),
+    "ek_selftest_xsum": (_I, [_L, _P, _I, _I, _P, _P, _P]),
     "ek_grid_len": (_L, [C.POINTER(Grid)]),
     "ek_workspace_bytes": (_L, [C.POINTER(Grid)]),
     "ek_copy": (_I, [_P, _P, _L, _I, _P]),

@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include "../../include/expkit_sm100.h"
+#include "ek_xsum.cuh"
 
 namespace ek {
 
@@ -101,6 +102,86 @@ __device__ __forceinline__ void gather_partials(const double* work, long nb, dou
         for (int q = 0; q < NQ; ++q) tot[q] += __ldcg(work + b * NQ + q);
     }
     block_sum<NQ, NT / 32>(tot);
+}
+
+// Grid-wide reduction of NQ fp64 channels, of which the first NX are real
+// sums: block partials -> ticket -> the last block totals them (tot[],
+// valid in its thread 0; returns true in every thread of that block). In
+// `repro` mode the first NX channels are taken from the integer
+// accumulators xs[] instead (ek_xsum.cuh): their block partials follow the
+// fp64 ones in `work` (nblocks * NQ doubles, then nblocks * NX * XSLOTS
+// slots), the last block merges them (any order gives the same bits) and
+// tot[q] = xvalue(xt[q]) for q < NX.
+// The two repro-mode steps are out of line (called once per thread, after
+// the kernel's main loop) and take copies of the accumulators, so the
+// integer merge code does not raise the register count of the kernels.
+template <int NX, int NT>
+__device__ __noinline__ void xpublish(const XAcc* xs_in, long long* xwork) {
+    XAcc xs[NX];
+#pragma unroll
+    for (int q = 0; q < NX; ++q) xs[q] = xs_in[q];
+    block_xsum<NX, NT / 32>(xs);
+    if (flat_tid() == 0) {
+        const long b = flat_bid();
+#pragma unroll
+        for (int q = 0; q < NX; ++q) xstore(xwork + (b * NX + q) * XSLOTS, xs[q]);
+    }
+}
+template <int NX, int NT>
+__device__ __noinline__ void xgather(const long long* xwork, long nb, XAcc* xt_out, double* tot) {
+    const int t = flat_tid();
+    XAcc xt[NX];
+#pragma unroll
+    for (int q = 0; q < NX; ++q) xzero(xt[q]);
+    for (long b = t; b < nb; b += NT) {
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            XAcc y;
+            const long long* src = xwork + (b * NX + q) * XSLOTS;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) y.a[i] = __ldcg(src + i);
+            y.top = (int)__ldcg(src + 4);
+            xmerge(xt[q], y);
+        }
+    }
+    block_xsum<NX, NT / 32>(xt);
+    if (t == 0) {
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            tot[q] = xvalue(xt[q]);
+            xt_out[q] = xt[q];
+        }
+    }
+}
+
+template <int NQ, int NX, int NT = TPB>
+__device__ __forceinline__ bool reduce_grid(double (&acc)[NQ], XAcc (&xs)[NX], bool repro,
+                                            double* work, uint32_t* ticket, bool sys,
+                                            double (&tot)[NQ], XAcc (&xt)[NX]) {
+    block_sum<NQ, NT / 32>(acc);
+    const long nb = nblocks();
+    long long* xwork = reinterpret_cast<long long*>(work + nb * NQ);
+    if (repro) {
+        XAcc tmp[NX];
+#pragma unroll
+        for (int q = 0; q < NX; ++q) tmp[q] = xs[q];
+        xpublish<NX, NT>(tmp, xwork);
+    }
+    if (!publish_and_arrive<NQ>(acc, work, ticket, sys)) return false;
+    gather_partials<NQ, NT>(work, nb, tot);
+    if (repro) {
+        XAcc tmp[NX];
+        double tv[NX];
+        xgather<NX, NT>(xwork, nb, tmp, tv);
+        if (flat_tid() == 0) {
+#pragma unroll
+            for (int q = 0; q < NX; ++q) {
+                tot[q] = tv[q];
+                xt[q] = tmp[q];
+            }
+        }
+    }
+    return true;
 }
 
 // Division by a launch-uniform divisor: reciprocal r = RN(1/d) plus one

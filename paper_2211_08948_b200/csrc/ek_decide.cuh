@@ -92,14 +92,23 @@ __device__ inline void power_decide(ek_power_state* st, double ssq, double bad, 
     st->nw = nw;
 }
 
-// Slab mode: rank-ordered global sums of the gathered part[] pairs.
+// Slab mode: global sums of the gathered part[] blocks (EK_PART_SLOTS
+// slots per rank, see EK_PART_*): the sum channel as the exact merge of the
+// ranks' integer accumulators (repro mode: any P gives the same bits), else
+// as the rank-ordered fp64 sum; the count channel in rank order.
 __device__ inline void gathered_sums(const double* g, int nranks, double& s0, double& s1) {
     s0 = 0.0;
     s1 = 0.0;
+    const bool xs = g[EK_PART_TAG] != 0.0;
+    XAcc tot;
+    xzero(tot);
     for (int r = 0; r < nranks; ++r) {
-        s0 = r == 0 ? g[0] : s0 + g[2 * r];
-        s1 += g[2 * r + 1];
+        const double* p = g + (long)r * EK_PART_SLOTS;
+        if (xs) xmerge(tot, xload(reinterpret_cast<const long long*>(p)));
+        else s0 = r == 0 ? p[0] : s0 + p[0];
+        s1 += p[EK_PART_COUNT];
     }
+    if (xs) s0 = xvalue(tot);
 }
 
 }  // namespace ek

@@ -149,7 +149,7 @@ __device__ __forceinline__ void issue_row(const KArgs& a, double* buf, uint64_t*
 template <class P, int EV, int EP, int K>
 __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                              const double* pc, const double* pp, long i, int j,
-                                             int t, int cols, double* acc) {
+                                             int t, int cols, double* acc, XAcc* xs) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     Nb nb[NC][NCH];
@@ -193,7 +193,7 @@ __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, con
     }
     double val[NC];
     evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val, z.jbad);
-    epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, z, acc);
+    epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, z, acc, xs);
 }
 
 // Strips across the row length; segments per strip for a grid of G blocks.
@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
     __syncthreads();
 
     double acc[NQ];
+    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
+    xzero(xs[0]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
             }
         }
         __syncwarp();
-        reduce_and_finalize<EV, EP, NQ, NT2>(a, acc);
+        reduce_and_finalize<EV, EP, NQ, NT2>(a, acc, xs);
         return;
     }
 #endif
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
             const double* pc = smem + sc * SD;
             const double* pp = smem + sp * SD;
             const long i = it.r0 + p - 1;
-            if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc);
+            if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs);
             release(q0 + p - 1, it, p - 1);
             sm = sc;
             sc = sp;
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
         release(q0 + it.L + 1, it, it.L + 1);
         q0 += it.L + 2;
     }
-    reduce_and_finalize<EV, EP, NQ, NT2>(a, acc);
+    reduce_and_finalize<EV, EP, NQ, NT2>(a, acc, xs);
 }
 
 }  // namespace ek

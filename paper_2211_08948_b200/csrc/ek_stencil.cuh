@@ -262,6 +262,9 @@ struct KArgs {
     // pre->val[1] = ||k - u_n||, pre->flag bit0 = k != u_n; *nu = ||u_n||
     const ek_scalar_state* pre;
     const double* nu;
+    // reproducible sums (ek_set_repro, ek_xsum.cuh): the norm channel of the
+    // reducing epilogues is accumulated in integers, independent of order
+    int repro;
 };
 
 // ----------------------------------------------------------------- geometry
@@ -306,6 +309,7 @@ struct Ctl {
     double* h_penult;
     double* h_last;
     long rowlen;
+    bool repro;           // order-independent sum channel (ek_xsum.cuh)
 };
 
 // Halo slot [ncomp][rowlen] of (rank r, parity, side) in the peer windows.
@@ -427,6 +431,7 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     ctl.shift = 0.0;
     ctl.y_zero = false;
     ctl.pinit = true;
+    ctl.repro = a.repro != 0;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(ctl.wpol));
     if constexpr (EP == EP_LEJA) {
         const ek_leja_state* st = (const ek_leja_state*)a.st;
@@ -573,7 +578,7 @@ __device__ __forceinline__ void st_stream(double* p, double v, uint64_t pol) {
 template <int EV, int EP, int NC, int K>
 __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long off,
                                          const double (&val)[NC],
-                                         const Centre<EV, EP, NC, K>& z, double* acc) {
+                                         const Centre<EV, EP, NC, K>& z, double* acc, XAcc* xs) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         const long e = c * a.npts + off;
@@ -583,7 +588,8 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
         } else if constexpr (EP == EP_RHSN) {
             st_stream(a.out + e, v, ctl.wpol);
             const double uc = z.y[c];
-            acc[0] += uc * uc;
+            if (ctl.repro) xadd<false>(xs[0], uc * uc);
+            else acc[0] += uc * uc;
             acc[1] += uc != 0.0 ? 1.0 : 0.0;
             acc[2] += isfinite(uc) ? 0.0 : 1.0;
         } else if constexpr (EP == EP_LEJA) {
@@ -591,7 +597,8 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             const double yn = dv(v, a.gamma) - (ctl.shift * z.y[c]);
             st_stream(a.out + e, yn, ctl.wpol);
             if (ctl.rowlen) peer_halo_store(a, ctl, off, c, yn);
-            acc[0] += yn * yn;
+            if (ctl.repro) xadd<false>(xs[0], yn * yn);
+            else acc[0] += yn * yn;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
 #pragma unroll
             for (int q = 0; q < K; ++q) {
@@ -608,7 +615,8 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             }
         } else if constexpr (EP == EP_POWER) {
             st_stream(a.out + e, v, ctl.wpol);
-            acc[0] += v * v;
+            if (ctl.repro) xadd<false>(xs[0], v * v);
+            else acc[0] += v * v;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
         } else if constexpr (EP == EP_ARN) {
             // V[j,:n] = op.apply(V[j-1,:n]) + V[j-1,n:] @ u_flip    kiops.py:182
@@ -643,9 +651,10 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
     }
 }
 
-// Last-block bookkeeping of one fused pass.
+// Last-block bookkeeping of one fused pass. `xt`: the order-independent
+// total of the sum channel (repro mode; tot[0] already holds its value).
 template <int EV, int EP>
-__device__ void finalize(const KArgs& a, const double* tot);
+__device__ void finalize(const KArgs& a, const double* tot, const XAcc& xt);
 
 template <int EP>
 __device__ __forceinline__ uint32_t* ticket_of(const KArgs& a) {
@@ -655,16 +664,22 @@ __device__ __forceinline__ uint32_t* ticket_of(const KArgs& a) {
     else return &((ek_scalar_state*)a.st)->ticket;
 }
 
+// Epilogues whose channel 0 is a sum of squares that repro mode takes over.
+__host__ __device__ constexpr bool ep_xsum(int ep) {
+    return ep == EP_LEJA || ep == EP_POWER || ep == EP_RHSN;
+}
+
 template <int EV, int EP, int NQ, int NT = TPB>
-__device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc)[NQ]) {
+__device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc)[NQ],
+                                                    XAcc (&xs)[1]) {
     if constexpr (ep_nq(EP) > 0) {
-        block_sum<NQ, NT / 32>(acc);
         // peer mode: this block's halo stores must reach the peers before
         // the last block raises the pass flag (system-scope fence)
-        if (publish_and_arrive<NQ>(acc, a.work, ticket_of<EP>(a), a.peer != nullptr)) {
-            double tot[NQ];
-            gather_partials<NQ, NT>(a.work, nblocks(), tot);
-            if (flat_tid() == 0) finalize<EV, EP>(a, tot);
+        double tot[NQ];
+        XAcc xt[1];
+        if (reduce_grid<NQ, 1, NT>(acc, xs, ep_xsum(EP) && a.repro != 0, a.work, ticket_of<EP>(a),
+                                   a.peer != nullptr, tot, xt)) {
+            if (flat_tid() == 0) finalize<EV, EP>(a, tot, xt[0]);
         }
     }
 }
@@ -683,6 +698,8 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
     const long tile_rows = 8L * RPT;
     const long ntiles = tiles_c * ((rows + tile_rows - 1) / tile_rows);
     double acc[NQ];
+    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
+    xzero(xs[0]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -750,11 +767,11 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
             if (i < rows && j < cols) {
                 double val[NC];
                 evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val, zc[r - 1].jbad);
-                epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, zc[r - 1], acc);
+                epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, zc[r - 1], acc, xs);
             }
         }
     }
-    reduce_and_finalize<EV, EP, NQ>(a, acc);
+    reduce_and_finalize<EV, EP, NQ>(a, acc, xs);
 }
 
 // ------------------------------------------------------------ 3-D kernel
@@ -770,6 +787,8 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
     const long tk = (n + 31) / 32, tj = (n + 7) / 8, ti = (rows + RPT - 1) / RPT;
     const long ntiles = tk * tj * ti;
     double acc[NQ];
+    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
+    xzero(xs[0]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -842,19 +861,31 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
             if (i < rows && kx < n && jy < n) {
                 double val[NC];
                 evaluate<P, EV, NCH>(a, ctl, nb, zc[r - 1].fu, val, zc[r - 1].jbad);
-                epilogue<EV, EP, NC, K>(a, ctl, i * plane + jy * n + kx, val, zc[r - 1], acc);
+                epilogue<EV, EP, NC, K>(a, ctl, i * plane + jy * n + kx, val, zc[r - 1], acc, xs);
             }
         }
     }
-    reduce_and_finalize<EV, EP, NQ>(a, acc);
+    reduce_and_finalize<EV, EP, NQ>(a, acc, xs);
 }
 
 // --------------------------------------------------------------- finalize
 
+// Slab mode: leave a pass's local sums in part[] (EK_PART_*): the sum
+// channel as one double, or in repro mode as the integer accumulator.
+__device__ __forceinline__ void part_store(double* part, const KArgs& a, double ssq,
+                                           const XAcc& xt, double count) {
+    if (a.repro) xstore(reinterpret_cast<long long*>(part), xt);
+    else part[0] = ssq;
+    part[EK_PART_COUNT] = count;
+    part[EK_PART_TAG] = a.repro ? 1.0 : 0.0;
+}
+
 template <int EV, int EP>
-__device__ void finalize(const KArgs& a, const double* tot) {
+__device__ void finalize(const KArgs& a, const double* tot, const XAcc& xt) {
     if constexpr (EP == EP_RHSN) {
         ek_scalar_state* st = (ek_scalar_state*)a.st;
+        if (a.repro) xstore((long long*)st->xs, xt);
+        st->repro = a.repro;
         st->val[0] = tot[0];
         st->val[1] = sqrt(tot[0]);
         st->flag |= (tot[1] > 0.0 ? 1 : 0) | (tot[2] > 0.0 ? 2 : 0);
@@ -867,9 +898,9 @@ __device__ void finalize(const KArgs& a, const double* tot) {
             const ek_peer* P = a.peer;
             const int par = (int)(a.epoch & 1);
             for (int r = 0; r < P->world; ++r) {
-                double* red = (double*)((char*)P->win[r] + 64) + (par * 8 + P->rank) * 2;
-                red[0] = tot[0];
-                red[1] = tot[1];
+                double* red = (double*)((char*)P->win[r] + 64) +
+                              (par * 8 + P->rank) * EK_PART_SLOTS;
+                part_store(red, a, tot[0], xt, tot[1]);
             }
             __threadfence_system();
             for (int r = 0; r < P->world; ++r) {
@@ -881,16 +912,14 @@ __device__ void finalize(const KArgs& a, const double* tot) {
             return;
         }
         if (st->defer) {  // slab mode: ek_leja_decide finishes with global sums
-            st->part[0] = tot[0];
-            st->part[1] = tot[1];
+            part_store(st->part, a, tot[0], xt, tot[1]);
             return;
         }
         leja_decide(st, a.coef, a.mi, a.m, a.nk, tot[0], tot[1], EV == EV_FD);
     } else if constexpr (EP == EP_POWER) {
         ek_power_state* st = (ek_power_state*)a.st;
         if (st->defer) {
-            st->part[0] = tot[0];
-            st->part[1] = tot[1];
+            part_store(st->part, a, tot[0], xt, tot[1]);
             return;
         }
         power_decide(st, tot[0], tot[1], EV == EV_FD);

@@ -193,7 +193,7 @@ template <class P, int EV, int EP, int K, bool EDGE>
 __device__ __forceinline__ void tma_point(const KArgs& a, const Ctl& ctl, const double* raw,
                                           const double* ctr, const double* const (&rb)[2],
                                           const double* const (&rh)[2], int i, int j, int wid,
-                                          int lane, int rows, int cols, double* acc) {
+                                          int lane, int rows, int cols, double* acc, XAcc* xs) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     const bool gx_m = EDGE && i == 0, gx_p = EDGE && i == rows - 1;  // ghost rows (warp-uniform)
@@ -247,7 +247,7 @@ __device__ __forceinline__ void tma_point(const KArgs& a, const Ctl& ctl, const 
     }
     double val[NC];
     evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val, z.jbad);
-    epilogue<EV, EP, NC, K>(a, ctl, (long)i * cols + j, val, z, acc);
+    epilogue<EV, EP, NC, K>(a, ctl, (long)i * cols + j, val, z, acc, xs);
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -321,6 +321,8 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
     __syncthreads();
 
     double acc[NQ];
+    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
+    xzero(xs[0]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -349,13 +351,13 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
         const double* ctr = raw + NR * NC * RAW_SLOT;
         mbar_wait(&full[s], (uint32_t)((k / S) & 1));
         if (r0 >= 1 && r0 + 8 < rows && j0 >= 1 && j0 + 32 < cols)
-            tma_point<P, EV, EP, K, false>(a, ctl, raw, ctr, rb, rh, i, j, wid, lane, rows, cols, acc);
+            tma_point<P, EV, EP, K, false>(a, ctl, raw, ctr, rb, rh, i, j, wid, lane, rows, cols, acc, xs);
         else if (i < rows && j < cols)
-            tma_point<P, EV, EP, K, true>(a, ctl, raw, ctr, rb, rh, i, j, wid, lane, rows, cols, acc);
+            tma_point<P, EV, EP, K, true>(a, ctl, raw, ctr, rb, rh, i, j, wid, lane, rows, cols, acc, xs);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     }
-    reduce_and_finalize<EV, EP, NQ>(a, acc);
+    reduce_and_finalize<EV, EP, NQ>(a, acc, xs);
 }
 
 }  // namespace ek

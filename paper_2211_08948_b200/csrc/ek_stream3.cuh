@@ -178,7 +178,7 @@ template <class P, int EV, int EP, int K, int IY, int EDGE>
 __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                            const double* pc, const double* pp,
                                            int ly, int lx, int jy, int kx, int ro, int co, int n,
-                                           long off, double* acc, int zpm, int zpp) {
+                                           long off, double* acc, XAcc* xs, int zpm, int zpp) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     constexpr int RAW3 = raw3(IY), CTR3 = ctr3(IY);
@@ -245,7 +245,7 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
     }
     double val[NC];
     evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val, z.jbad);
-    epilogue<EV, EP, NC, K>(a, ctl, off, val, z, acc);
+    epilogue<EV, EP, NC, K>(a, ctl, off, val, z, acc, xs);
 }
 
 
@@ -310,6 +310,8 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
     __syncthreads();
 
     double acc[NQ];
+    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
+    xzero(xs[0]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
             }
         }
         __syncwarp();
-        reduce_and_finalize<EV, EP, NQ, NT3>(a, acc);
+        reduce_and_finalize<EV, EP, NQ, NT3>(a, acc, xs);
         return;
     }
 #endif
@@ -407,19 +409,19 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
                 const int ro = (1 + ly) * TBW3 + 2 + lx, co = ly * I3X + lx;
                 if (edge == 0)
                     tma3_point<P, EV, EP, K, IY, 0>(a, ctl, pm, pc, pp, ly, lx, jy, kx, ro,
-                                                    co, n, off[r], acc, zpm, zpp);
+                                                    co, n, off[r], acc, xs, zpm, zpp);
                 else if (jy < n && kx < n) {
                     // y-edge items: only the rows j = 0 / n-1 need the selects
                     const int e = edge & ~((jy > 0 && jy < n - 1) ? 1 : 0);
                     if (e == 2)
                         tma3_point<P, EV, EP, K, IY, 2>(a, ctl, pm, pc, pp, ly, lx, jy, kx,
-                                                        ro, co, n, off[r], acc, zpm, zpp);
+                                                        ro, co, n, off[r], acc, xs, zpm, zpp);
                     else if (e == 0)
                         tma3_point<P, EV, EP, K, IY, 0>(a, ctl, pm, pc, pp, ly, lx, jy, kx,
-                                                        ro, co, n, off[r], acc, zpm, zpp);
+                                                        ro, co, n, off[r], acc, xs, zpm, zpp);
                     else
                         tma3_point<P, EV, EP, K, IY, 3>(a, ctl, pm, pc, pp, ly, lx, jy, kx,
-                                                        ro, co, n, off[r], acc, zpm, zpp);
+                                                        ro, co, n, off[r], acc, xs, zpm, zpp);
                 }
                 off[r] += plane;
             }
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
         release(q0 + it.L + 1, t, it, it.L + 1);
         q0 += it.L + 2;
     }
-    reduce_and_finalize<EV, EP, NQ, NT3>(a, acc);
+    reduce_and_finalize<EV, EP, NQ, NT3>(a, acc, xs);
 }
 
 }  // namespace ek

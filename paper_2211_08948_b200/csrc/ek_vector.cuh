@@ -65,8 +65,10 @@ __device__ __forceinline__ void st4(double* x, int64_t e0, int64_t len, bool ful
 // = ssq, st->val[slot+1] = sqrt(ssq). `div` (nullable) scales on read.
 __global__ void __launch_bounds__(TPB) k_norm2(int64_t len, const double* __restrict__ x,
                                                const double* div, ek_scalar_state* st,
-                                               int slot, double* work) {
+                                               int slot, double* work, int repro) {
     double acc[3] = {0.0, 0.0, 0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
     const double d = div ? *div : 1.0;
     const bool has_div = div != nullptr, vec = al16d(x);
     EK_FOR4(e0, len) {
@@ -76,16 +78,20 @@ __global__ void __launch_bounds__(TPB) k_norm2(int64_t len, const double* __rest
         for (int w = 0; w < 4; ++w) {
             if (e0 + w >= len) break;
             if (has_div) v[w] = v[w] / d;
-            acc[0] += v[w] * v[w];
+            if (repro) xadd<false>(xs[0], v[w] * v[w]);
+            else acc[0] += v[w] * v[w];
             acc[1] += (v[w] != 0.0) ? 1.0 : 0.0;
             acc[2] += isfinite(v[w]) ? 0.0 : 1.0;
         }
     }
-    block_sum<3>(acc);
-    if (publish_and_arrive<3>(acc, work, &st->ticket)) {
-        double tot[3];
-        gather_partials<3>(work, gridDim.x, tot);
+    double tot[3];
+    XAcc xt[1];
+    if (reduce_grid<3, 1>(acc, xs, repro != 0, work, &st->ticket, false, tot, xt)) {
         if (threadIdx.x == 0) {
+            if (slot == 0) {
+                if (repro) xstore((long long*)st->xs, xt[0]);
+                st->repro = repro;
+            }
             st->val[slot] = tot[0];
             st->val[slot + 1] = sqrt(tot[0]);
             st->flag |= (tot[1] > 0.0 ? 1 : 0) | (tot[2] > 0.0 ? 2 : 0);
@@ -126,7 +132,16 @@ struct LejaVArgs {
     double gamma;
     ek_leja_state* st;
     double* work;
+    int repro;            // order-independent ||.||^2 (ek_xsum.cuh)
 };
+
+// Slab mode: a vector pass leaves its local sum in part[] (EK_PART_*).
+__device__ __forceinline__ void part_store_v(double* part, int repro, double ssq, const XAcc& xt) {
+    if (repro) xstore(reinterpret_cast<long long*>(part), xt);
+    else part[0] = ssq;
+    part[EK_PART_COUNT] = 0.0;
+    part[EK_PART_TAG] = repro ? 1.0 : 0.0;
+}
 
 // Initialise a Leja state block on the device (ek_leja_call): the host
 // values travel as kernel arguments, ||u|| optionally from a device slot.
@@ -149,6 +164,8 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
     // Every block reads the flag before the last one rewrites it.
     const bool fold = a.st->p_init < 0;
     double acc[1] = {0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
     double d[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
@@ -172,14 +189,20 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int w = 0; w < 4; ++w) acc[0] += y[u][w] * y[u][w];
+                for (int w = 0; w < 4; ++w) {
+                    if (a.repro) xadd<false>(xs[0], y[u][w] * y[u][w]);
+                    else acc[0] += y[u][w] * y[u][w];
+                }
         }
     } else EK_FOR4(e0, a.len) {
         const bool full = vec && e0 + 4 <= a.len;
         double y[4];
         ld4(a.b, e0, a.len, full, y);
 #pragma unroll
-        for (int w = 0; w < 4; ++w) acc[0] += y[w] * y[w];  // zeros past len
+        for (int w = 0; w < 4; ++w) {  // zeros past len
+            if (a.repro) xadd<false>(xs[0], y[w] * y[w]);
+            else acc[0] += y[w] * y[w];
+        }
         {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -191,15 +214,13 @@ __global__ void __launch_bounds__(TPB) k_leja_begin(const LejaVArgs a) {
                 }
         }
     }
-    block_sum<1>(acc);
-    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
-        double tot[1];
-        gather_partials<1>(a.work, gridDim.x, tot);
+    double tot[1];
+    XAcc xt[1];
+    if (reduce_grid<1, 1>(acc, xs, a.repro != 0, a.work, &a.st->ticket, false, tot, xt)) {
         if (threadIdx.x == 0) {
             a.st->p_init = fold ? 0 : 1;
             if (a.st->defer) {
-                a.st->part[0] = tot[0];
-                a.st->part[1] = 0.0;
+                part_store_v(a.st->part, a.repro, tot[0], xt[0]);
             } else {
                 leja_begin_decide(a.st, a.coef, a.nk, tot[0]);
             }
@@ -292,7 +313,7 @@ __global__ void __launch_bounds__(TPB) k_dot_multi(const DotArgs a) {
 }
 
 // Slab mode: apply a deferred Leja decision to the gathered per-rank sums
-// (`g` = [nranks][2] part[] pairs, summed in rank order).
+// (`g` = [nranks][EK_PART_SLOTS] part[] blocks, see gathered_sums).
 __global__ void k_leja_decide(ek_leja_state* st, const double* g, int nranks, const double* coef,
                               int mi, int m, int nk, int fd, int begin) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -338,7 +359,8 @@ __global__ void k_peer_decide(ek_leja_state* st, const ek_peer* P, long epoch, c
         return;
     }
     double s0, s1;
-    gathered_sums((const double*)((const char*)win + 64) + (epoch & 1) * 16, P->world, s0, s1);
+    gathered_sums((const double*)((const char*)win + 64) + (epoch & 1) * 8 * EK_PART_SLOTS,
+                  P->world, s0, s1);
     leja_decide(st, coef, mi, m, nk, s0, s1, fd != 0);
 }
 
@@ -368,23 +390,24 @@ __global__ void __launch_bounds__(TPB) k_leja_update(const LejaVArgs a) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
     double acc[1] = {0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
     for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
          e += (int64_t)gridDim.x * TPB) {
         const double yn = dv(__ldg(a.b + e), gam) - (shift * __ldg(a.y + e));
         a.ynext[e] = yn;
-        acc[0] += yn * yn;
+        if (a.repro) xadd<false>(xs[0], yn * yn);
+        else acc[0] += yn * yn;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
             if (q < a.nk && ((act >> q) & 1u)) a.p[q][e] = a.p[q][e] + (d[q] * yn);
     }
-    block_sum<1>(acc);
-    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
-        double tot[1];
-        gather_partials<1>(a.work, gridDim.x, tot);
+    double tot[1];
+    XAcc xt[1];
+    if (reduce_grid<1, 1>(acc, xs, a.repro != 0, a.work, &a.st->ticket, false, tot, xt)) {
         if (threadIdx.x == 0) {
             if (a.st->defer) {
-                a.st->part[0] = tot[0];
-                a.st->part[1] = 0.0;
+                part_store_v(a.st->part, a.repro, tot[0], xt[0]);
             } else {
                 // the Jacobian action was checked by its own operator
                 leja_decide(a.st, a.coef, a.mi, a.m, a.nk, tot[0], 0.0, false);
@@ -664,10 +687,12 @@ __global__ void __launch_bounds__(TPB) k_basis_combine(const CombineArgs a) {
 // ||v0|| -> st->nw (the divisor of the first iterate), FD: ||v0/||v0|| || -> nv
 __global__ void __launch_bounds__(TPB) k_power_norm(int64_t len, const double* __restrict__ x,
                                                     int scaled, ek_power_state* st,
-                                                    double* work) {
+                                                    double* work, int repro) {
     if (scaled && (st->done || st->status)) return;
     const Dv d = mkdv(st->nw);
     double acc[1] = {0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
     const bool vec = al16d(x);
     EK_FOR4(e0, len) {
         double v[4];
@@ -676,17 +701,16 @@ __global__ void __launch_bounds__(TPB) k_power_norm(int64_t len, const double* _
         for (int w = 0; w < 4; ++w) {
             if (e0 + w >= len) break;
             if (scaled) v[w] = dv(v[w], d);
-            acc[0] += v[w] * v[w];
+            if (repro) xadd<false>(xs[0], v[w] * v[w]);
+            else acc[0] += v[w] * v[w];
         }
     }
-    block_sum<1>(acc);
-    if (publish_and_arrive<1>(acc, work, &st->ticket)) {
-        double tot[1];
-        gather_partials<1>(work, gridDim.x, tot);
+    double tot[1];
+    XAcc xt[1];
+    if (reduce_grid<1, 1>(acc, xs, repro != 0, work, &st->ticket, false, tot, xt)) {
         if (threadIdx.x == 0) {
             if (st->defer) {
-                st->part[0] = tot[0];
-                st->part[1] = 0.0;
+                part_store_v(st->part, repro, tot[0], xt[0]);
             } else if (scaled) {
                 st->nv = sqrt(tot[0]);
             } else {
@@ -719,9 +743,13 @@ struct VexprArgs {
     ek_scalar_state* st;
     double* work;
     int reduce;  // 1 if the program has NORM/CHECK ops
+    int repro;   // order-independent NORM / ACC channels (ek_xsum.cuh)
 };
 __global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};  // 0,1: norms ; 2: nonzero ; 3: non-finite
+    XAcc xs[2];
+    xzero(xs[0]);
+    xzero(xs[1]);
     for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < a.len;
          e += (int64_t)gridDim.x * TPB) {
         double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0;  // register stack
@@ -755,9 +783,13 @@ __global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
                 case VX_POP: --sp; break;
                 case VX_NORM: {
                     const double t = VX_AT(sp - 1);
-                    acc[arg] += t * t;
+                    if (a.repro) xadd<false>(xs[arg & 1], t * t);
+                    else acc[arg] += t * t;
                 } break;
-                case VX_ACC: acc[arg] += VX_AT(sp - 1); break;
+                case VX_ACC:
+                    if (a.repro) xadd<true>(xs[arg & 1], VX_AT(sp - 1));
+                    else acc[arg] += VX_AT(sp - 1);
+                    break;
                 case VX_CHECK: {
                     const double t = VX_AT(sp - 1);
                     acc[2] += t != 0.0 ? 1.0 : 0.0;
@@ -780,11 +812,12 @@ __global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
 #undef VX_AT
     }
     if (a.reduce) {
-        block_sum<4>(acc);
-        if (publish_and_arrive<4>(acc, a.work, &a.st->ticket)) {
-            double tot[4];
-            gather_partials<4>(a.work, gridDim.x, tot);
+        double tot[4];
+        XAcc xt[2];
+        if (reduce_grid<4, 2>(acc, xs, a.repro != 0, a.work, &a.st->ticket, false, tot, xt)) {
             if (threadIdx.x == 0) {
+                if (a.repro) xstore((long long*)a.st->xs, xt[0]);
+                a.st->repro = a.repro;
                 a.st->val[0] = tot[0];
                 a.st->val[1] = sqrt(tot[0]);
                 a.st->val[2] = tot[1];
@@ -818,6 +851,7 @@ struct LincombArgs {
     int reduce;
     ek_scalar_state* st;
     double* work;
+    int repro;  // order-independent ||out0||^2 (ek_xsum.cuh)
 };
 
 __device__ __forceinline__ double lc_term(const LincombArgs& a, int o, int t, double x) {
@@ -834,6 +868,8 @@ template <int NOUT, bool ALIGNED>
 __global__ void __launch_bounds__(TPB) k_lincomb(const LincombArgs a) {
     constexpr int W = 4;
     double red[3] = {0.0, 0.0, 0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
     const int64_t ngroups = (a.len + W - 1) / W;
     for (int64_t gi = (int64_t)blockIdx.x * TPB + threadIdx.x; gi < ngroups;
          gi += (int64_t)gridDim.x * TPB) {
@@ -894,7 +930,8 @@ __global__ void __launch_bounds__(TPB) k_lincomb(const LincombArgs a) {
 #pragma unroll
             for (int w = 0; w < W; ++w) {
                 if (e0 + w < a.len) {
-                    red[0] += r[w] * r[w];
+                    if (a.repro) xadd<false>(xs[0], r[w] * r[w]);
+                    else red[0] += r[w] * r[w];
                     red[1] += r[w] != 0.0 ? 1.0 : 0.0;
                     red[2] += isfinite(r[w]) ? 0.0 : 1.0;
                 }
@@ -902,11 +939,12 @@ __global__ void __launch_bounds__(TPB) k_lincomb(const LincombArgs a) {
         }
     }
     if (a.reduce) {
-        block_sum<3>(red);
-        if (publish_and_arrive<3>(red, a.work, &a.st->ticket)) {
-            double tot[3];
-            gather_partials<3>(a.work, gridDim.x, tot);
+        double tot[3];
+        XAcc xt[1];
+        if (reduce_grid<3, 1>(red, xs, a.repro != 0, a.work, &a.st->ticket, false, tot, xt)) {
             if (threadIdx.x == 0) {
+                if (a.repro) xstore((long long*)a.st->xs, xt[0]);
+                a.st->repro = a.repro;
                 a.st->val[0] = tot[0];
                 a.st->val[1] = sqrt(tot[0]);
                 a.st->flag |= (tot[1] > 0.0 ? 1 : 0) | (tot[2] > 0.0 ? 2 : 0);

@@ -34,6 +34,7 @@ int cuda_status(cudaError_t e, const char* where) {
 static std::atomic<long long> g_launches{0};
 int g_tma_mode = 3;  // see ek_set_tma
 int g_march_mask = 1 << EP_LEJA;  // see ek_set_march
+int g_repro = 0;  // see ek_set_repro: order-independent sums (ek_xsum.cuh)
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ------------------------------------------------------------- 1-D problem
@@ -173,6 +174,7 @@ static void base_args(KArgs& a, const ek_grid* g, const double* const* halo) {
     a.pc.h = mkdv(g->h);
     for (int i = 0; i < 8; ++i) a.pc.prm[i] = g->prm[i];
     a.gamma = mkdv(1.0);
+    a.repro = g_repro;
     if (halo) {
         a.hu = halo[0];
         a.hy = halo[1];
@@ -210,6 +212,29 @@ int ek_set_tma(int mode) {
     return old;
 }
 
+int ek_set_repro(int on) {
+    const int old = g_repro;
+    if (on >= 0) g_repro = on ? 1 : 0;
+    return old;
+}
+
+double ek_xsum_value(const int64_t* slots, int n) {
+    XAcc tot;
+    xzero(tot);
+    for (int r = 0; r < n; ++r) xmerge(tot, xload((const long long*)slots + (long)r * XSLOTS));
+    return xvalue(tot);
+}
+
+void ek_xsum_host(const double* x, int64_t n, int sq, int64_t* slots_out) {
+    XAcc acc;
+    xzero(acc);
+    for (int64_t i = 0; i < n; ++i) {
+        if (sq) xadd<false>(acc, x[i] * x[i]);
+        else xadd<true>(acc, x[i]);
+    }
+    xstore((long long*)slots_out, acc);
+}
+
 int ek_set_march(int mask) {
     const int old = g_march_mask;
     if (mask >= 0) g_march_mask = mask;
@@ -242,7 +267,9 @@ int64_t ek_workspace_bytes(const ek_grid* g) {
         const int64_t sb = (int64_t)sm_count() * 8;  // persistent stencil grids
         if (sb > nb) nb = sb;
     }
-    return nb * 8 * (int64_t)sizeof(double);
+    // per block: up to 8 fp64 partials, and in repro mode up to 8 integer
+    // accumulators of XSLOTS slots behind them
+    return nb * (8 + 8 * XSLOTS) * (int64_t)sizeof(double);
 }
 
 int ek_rhs(const ek_grid* g, const double* u, double* out, const double* const* halo,
@@ -303,7 +330,7 @@ int ek_jv(const ek_grid* g, int jac, const double* u, const double* fu, const do
     int rc = launch_stencil<EP_STORE>(ev, a, s);
     if (rc != EK_OK || jac != EK_JAC_FD || !st) return rc;
     // non-finite check of the FD result (linalg.py:127-128)
-    k_norm2<<<vgrid4(ek_grid_len(g)), TPB, 0, s>>>(ek_grid_len(g), out, nullptr, st, 6, work);
+    k_norm2<<<vgrid4(ek_grid_len(g)), TPB, 0, s>>>(ek_grid_len(g), out, nullptr, st, 6, work, 0);
     EK_LAUNCH_CHECK("k_norm2");
     return EK_OK;
 }
@@ -406,6 +433,7 @@ int ek_leja_begin_len(int64_t len, const double* b, double* const* p, int k,
     }
     LejaVArgs a{};
     a.len = len; a.b = b; a.nk = k; a.coef = coef_dev; a.mi = 0; a.m = 0; a.st = st; a.work = work;
+    a.repro = g_repro;
     for (int q = 0; q < k; ++q) a.p[q] = p[q];
     k_leja_begin<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(a);
     EK_LAUNCH_CHECK("k_leja_begin");
@@ -476,6 +504,7 @@ int ek_leja_update(int64_t len, const double* jv, const double* y, double* ynext
     LejaVArgs a{};
     a.len = len; a.b = jv; a.y = y; a.ynext = ynext; a.nk = k; a.coef = coef_dev;
     a.mi = m - chunk_base; a.m = m; a.gamma = gamma; a.st = st; a.work = work;
+    a.repro = g_repro;
     for (int q = 0; q < k; ++q) a.p[q] = p[q];
     k_leja_update<<<vgrid(len), TPB, 0, (cudaStream_t)stream>>>(a);
     EK_LAUNCH_CHECK("k_leja_update");
@@ -496,10 +525,10 @@ int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, c
     const bool slab = halo != nullptr;
     if (it_begin == 0 && !slab) {
         // v = v0 / ||v0||   (spectrum.py:49-51): divisor and, for FD, ||v||
-        k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, v0, 0, st, work);
+        k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, v0, 0, st, work, g_repro);
         EK_LAUNCH_CHECK("k_power_norm");
         if (jac == EK_JAC_FD) {
-            k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, v0, 1, st, work);
+            k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, v0, 1, st, work, g_repro);
             EK_LAUNCH_CHECK("k_power_norm");
         }
     }
@@ -512,7 +541,7 @@ int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, c
         const int rc = launch_stencil<EP_POWER>(ev, a, s);
         if (rc != EK_OK) return rc;
         if (jac == EK_JAC_FD && !slab) {
-            k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, a.out, 1, st, work);
+            k_power_norm<<<vgrid4(len), TPB, 0, s>>>(len, a.out, 1, st, work, g_repro);
             EK_LAUNCH_CHECK("k_power_norm");
         }
     }
@@ -521,7 +550,7 @@ int ek_power_run(const ek_grid* g, int jac, const double* u, const double* fu, c
 
 int ek_power_norm(int64_t len, const double* x, int scaled, ek_power_state* st, double* work,
                   void* stream) {
-    k_power_norm<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(len, x, scaled, st, work);
+    k_power_norm<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(len, x, scaled, st, work, g_repro);
     EK_LAUNCH_CHECK("k_power_norm");
     return EK_OK;
 }
@@ -861,6 +890,7 @@ int ek_vexpr(int64_t len, const int32_t* prog, int nprog, const double* scal, in
     VexprArgs a;
     memset(&a, 0, sizeof(a));
     a.len = len; a.nprog = nprog; a.st = st; a.work = work;
+    a.repro = g_repro;
     int reduce = 0;
     for (int i = 0; i < nprog; ++i) {
         a.prog[i] = prog[i];
@@ -886,7 +916,7 @@ int ek_norm2(int64_t len, const double* x, ek_scalar_state* st, int slot, double
         set_error("ek_norm2: slot %d", slot);
         return EK_ERR_INVALID;
     }
-    k_norm2<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(len, x, nullptr, st, slot, work);
+    k_norm2<<<vgrid4(len), TPB, 0, (cudaStream_t)stream>>>(len, x, nullptr, st, slot, work, g_repro);
     EK_LAUNCH_CHECK("k_norm2");
     return EK_OK;
 }
@@ -910,6 +940,7 @@ int ek_lincomb(int64_t len, const double* const* in, int nin, double* const* out
     memset(&a, 0, sizeof(a));
     a.len = len;
     a.nout = nout;
+    a.repro = g_repro;
     for (int i = 0; i < nin; ++i) a.in[i] = in[i];
     for (int o = 0; o < nout; ++o) {
         a.out[o] = out[o];
@@ -967,6 +998,48 @@ int ek_selftest_div(int64_t n, const double* x, const double* d, double* fast, d
                     void* stream) {
     k_selftest_div<<<vgrid(n), TPB, 0, (cudaStream_t)stream>>>(n, x, d, fast, exact);
     EK_LAUNCH_CHECK("k_selftest_div");
+    return EK_OK;
+}
+
+// Order-independent sum self-test: the sum of x (sq = 1: of its squares) by
+// a grid of `blocks` blocks, through the kernels' own reduce_grid path.
+// out_slots[EK_XSLOTS] (device) receives the merged accumulator, st->val[0]
+// its value.
+__global__ void __launch_bounds__(TPB) k_selftest_xsum(int64_t n, const double* __restrict__ x,
+                                                       int sq, ek_scalar_state* st,
+                                                       long long* out_slots, double* work) {
+    double acc[1] = {0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
+    for (int64_t e = (int64_t)blockIdx.x * TPB + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * TPB) {
+        if (sq) xadd<false>(xs[0], x[e] * x[e]);
+        else xadd<true>(xs[0], x[e]);
+    }
+    double tot[1];
+    XAcc xt[1];
+    if (reduce_grid<1, 1>(acc, xs, true, work, &st->ticket, false, tot, xt)) {
+        if (threadIdx.x == 0) {
+            st->val[0] = tot[0];
+            xstore(out_slots, xt[0]);
+        }
+    }
+}
+
+int ek_selftest_xsum(int64_t n, const double* x, int sq, int blocks, ek_scalar_state* st,
+                     int64_t* out_slots, void* stream) {
+    if (n < 0 || blocks < 1 || blocks > VGRID_MAX || !st || !out_slots) {
+        set_error("ek_selftest_xsum: bad arguments");
+        return EK_ERR_INVALID;
+    }
+    double* work = nullptr;
+    if (cudaMalloc(&work, (size_t)blocks * (1 + XSLOTS) * sizeof(double)) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "ek_selftest_xsum");
+    k_selftest_xsum<<<blocks, TPB, 0, (cudaStream_t)stream>>>(n, x, sq, st, (long long*)out_slots,
+                                                              work);
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(work);
+    if (e != cudaSuccess) return cuda_status(e, "ek_selftest_xsum");
     return EK_OK;
 }
 

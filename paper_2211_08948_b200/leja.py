@@ -321,9 +321,10 @@ class _CoefTable:
 
 
 def _part_view(st):
-    """The 2-double `part` field of a device state block, as a tensor."""
-    off = type(st.host).part.offset
-    return st.buf[off:off + 16].view(D.F64)
+    """The `part` field (EK_PART_SLOTS 8-byte slots) of a device state block,
+    as a tensor."""
+    fld = type(st.host).part
+    return st.buf[fld.offset:fld.offset + fld.size].view(D.F64)
 
 
 def _slab_decide(st, Jn, table, base, m, k, begin):

@@ -32,6 +32,7 @@ Activate with `distribute(problem)`; the returned Problem carries a local
 """
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -148,16 +149,20 @@ class SlabComm:
 
     # ------------------------------------------------------- reductions
     def allgather_pairs(self, part):
-        """[world, 2] device tensor of every rank's 2-double `part` view."""
+        """[world, k] device tensor of every rank's k-slot `part` view (the
+        EK_PART_SLOTS block of a control state: fp64 values, or in repro
+        mode the bit patterns of the integer accumulator — the gather only
+        moves bytes)."""
+        k = part.numel()
         if self.world == 1:
-            return part.reshape(1, 2)
+            return part.reshape(1, k)
         if self.host_staged:
-            bufs = [torch.empty(2, dtype=torch.float64) for _ in range(self.world)]
+            bufs = [torch.empty(k, dtype=torch.float64) for _ in range(self.world)]
             dist.all_gather(bufs, part.cpu(), group=self.group)
             return torch.stack(bufs).to(part.device)
-        out = torch.empty(self.world * 2, dtype=torch.float64, device=part.device)
+        out = torch.empty(self.world * k, dtype=torch.float64, device=part.device)
         dist.all_gather_into_tensor(out, part.contiguous(), group=self.group)
-        return out.reshape(self.world, 2)
+        return out.reshape(self.world, k)
 
     def allgather_vals(self, part):
         """[world * k] device tensor of every rank's k-double device view
@@ -191,6 +196,18 @@ class SlabComm:
                 s = s + rows[r][i]
             out.append(s)
         return out
+
+    def allgather_ints(self, values):
+        """[world][len(values)] host ints of every rank (int64 payload: the
+        slots of an order-independent accumulator, ek_xsum.cuh)."""
+        if self.world == 1:
+            return [list(values)]
+        t = torch.tensor(values, dtype=torch.int64)
+        if not self.host_staged:
+            t = t.cuda()
+        bufs = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(bufs, t, group=self.group)
+        return [b.cpu().tolist() for b in bufs]
 
     # --------------------------------------------------- data movement
     def scatter(self, u_global, grid_global):
@@ -295,6 +312,12 @@ def distribute(problem, comm=None):
     rhs.comm = comm
     rhs.global_grid = st.grid
     D.COMM = comm if comm.world > 1 else None
+    # every norm on the path is an order-independent
+    # sum, so results are bitwise identical for every decomposition (and for
+    # the whole-grid run under `_device.set_reproducible()`); EK_REPRO=0
+    # keeps the rank-ordered fp64 sums
+    if os.environ.get("EK_REPRO", "1") != "0":
+        D.set_reproducible(True)
     jf = NativeJacFactory(rhs) if isinstance(problem.jac_factory, NativeJacFactory) else None
     u0 = comm.scatter(problem.u0, st.grid)
     out = Problem(problem.name, rhs, u0, problem.t_final, n=problem.n,

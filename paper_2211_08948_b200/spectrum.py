@@ -103,8 +103,8 @@ def power_iterate(J: MatrixFreeOperator, tol_pi=1e-2, max_it=1000, seed=0):
 
 
 def _part(st):
-    off = type(st.host).part.offset
-    return st.buf[off:off + 16].view(D.F64)
+    fld = type(st.host).part
+    return st.buf[fld.offset:fld.offset + fld.size].view(D.F64)
 
 
 def _slab_decide(st, J, which):

@@ -71,10 +71,19 @@ def _emulated_peer_leja(grid, jac, u, fu, b, coeffs, l, h, est, tol, xi, P):
         rk["win"] = ptr.value
         ranks.append(rk)
     # ||u|| of the global field as the slab path forms it: rank-ordered sum
-    # of the ranks' sums of squares
-    nu = 0.0
-    for rk in ranks:
-        nu = nu + float(torch.sum(rk["u"] * rk["u"]))
+    # of the ranks' sums of squares; in repro mode the exact merge of the
+    # ranks' integer accumulators (ek_xsum_host is the kernels' per-term code)
+    if lib.ek_set_repro(-1):
+        slots = (C.c_int64 * (N.XSLOTS * P))()
+        for r, rk in enumerate(ranks):
+            ur = np.ascontiguousarray(rk["u"].cpu().numpy())
+            lib.ek_xsum_host(ur.ctypes.data_as(C.c_void_p), ur.size, 1,
+                             C.cast(C.byref(slots, 8 * N.XSLOTS * r), C.POINTER(C.c_int64)))
+        nu = lib.ek_xsum_value(slots, P)
+    else:
+        nu = 0.0
+        for rk in ranks:
+            nu = nu + float(torch.sum(rk["u"] * rk["u"]))
     nu = float(np.sqrt(nu)) if jac == N.JAC_FD else 0.0
     for r, rk in enumerate(ranks):
         up = r - 1 if r > 0 else (P - 1 if periodic else -1)
@@ -146,3 +155,44 @@ def test_peer_leja_emulated_ranks_match_whole_grid(name, n, jac, P):
     tol = 1e-13 if jac == N.JAC_ANALYTIC else 1e-7
     for g, r in zip(got, ref.vectors):
         assert np.linalg.norm(g - r) <= tol * np.linalg.norm(r)
+
+
+REPRO_CASES = [("advdiff2d", 64, N.JAC_ANALYTIC), ("brusselator_periodic", 64, N.JAC_FD),
+               ("allen_cahn", 64, N.JAC_FD), ("advdiff3d", 32, N.JAC_ANALYTIC)]
+
+
+@pytest.mark.parametrize("name,n,jac", REPRO_CASES)
+def test_repro_sums_make_the_leja_call_bitwise_identical_for_every_P(name, n, jac):
+    """with the order-independent sums (ek_set_repro) the
+    whole-grid fused call and the peer path at P = 1, 2, 4 give the same
+    bits — vectors, iterations and freeze points — for analytic and FD
+    Jacobians (through the FD increment every ulp of ||y|| would show)."""
+    xi = ek.get_leja_points(400)
+    old = D.set_reproducible(True)
+    try:
+        if name == "allen_cahn":
+            p = ek.make_problem("allen_cahn", n=n)
+        else:
+            p = ext.make_ext_problem(name, n=n)
+        jf = p.jac_factory if jac == N.JAC_ANALYTIC else None
+        rhs = ek.CountingRhs(p.rhs)
+        sys_ = ek.make_linearized(rhs, p.u0, jac_factory=jf)
+        est = ek.make_estimate(ek.power_iterate(sys_.J)[0])
+        dt = 20.0 / abs(est.alpha)
+        b = sys_.f_n * dt
+        coeffs = [0.5, 1.0]
+        ref = ek.leja_interpolate_vertical(sys_.J, b, 1, coeffs, dt, est, 1e-10, xi=xi)
+        assert 3 < ref.iters < 31
+        periodic = p.rhs.grid.bc == N.BC_PERIODIC
+        for P in ((1, 2, 4) if periodic else (2, 4)):
+            states, got = _emulated_peer_leja(p.rhs.grid, jac, p.u0, sys_.f_n, b, coeffs, 1, dt,
+                                              est, 1e-10, xi, P)
+            for h in states:
+                assert h.status == N.ST_OK and h.done
+                assert int(h.iters) == ref.iters
+                assert [int(h.freeze[i]) for i in range(2)] == ref.freeze_iters
+                assert h.ny == states[0].ny and h.eps == states[0].eps
+            for g, r in zip(got, ref.vectors):
+                assert np.array_equal(g, r), (P, np.abs(g - r).max())
+    finally:
+        D.set_reproducible(old)

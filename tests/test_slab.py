@@ -22,6 +22,22 @@ from paper_2211_08948_b200 import slab as S
 from paper_2211_08948_b200.problems import make_grid
 
 
+@pytest.fixture(autouse=True)
+def _restore_repro():
+    """`slab.distribute` switches the order-independent sums on for the
+    process; leave the default for the other test modules."""
+    yield
+    try:
+        N.lib().ek_set_repro(0)
+    except RuntimeError:
+        pass
+
+
+def _repro(on):
+    from paper_2211_08948_b200 import _device as D
+    return D.set_reproducible(on)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -131,6 +147,7 @@ def _gpu_run(local, n, comm=None, dim=2, name=None):
 @pytest.mark.parametrize("dim,n", [(2, 96), (3, 34)])
 def test_slab_path_p1_bit_identical(dim, n):
     from paper_2211_08948_b200 import _device as D
+    _repro(True)  # as the slab path: order-independent sums (same bits for every P)
     a = _gpu_run(0, n, dim=dim)
     b = _gpu_run(0, n, comm=S.SlabComm(), dim=dim)
     D.COMM = None
@@ -151,6 +168,7 @@ def test_peer_mode_p1_bit_identical(dim, n, name):
     rank is its own neighbour; reflect: it writes its own mirror ghosts):
     bit-identical to the whole-grid path, counts included."""
     from paper_2211_08948_b200 import _device as D
+    _repro(True)
     a = _gpu_run(0, n, dim=dim, name=name)
     comm = S.SlabComm(peer=True)
     assert comm.peer
@@ -200,6 +218,36 @@ def test_two_ranks_match_single_gpu(dim, n):
     # both ranks hold the same gathered results
     for x, y in zip(res[0]["vecs"], res[1]["vecs"]):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,n", [(2, 128), (3, 34)])
+def test_two_ranks_bitwise_equal_whole_grid_with_repro_sums(dim, n):
+    """with the order-independent sums the two-rank run
+    (power iteration, vertical Leja call, one EPIRK5P1 step with its FD
+    remainders and error norm) equals the whole-grid run bit for bit."""
+    _repro(True)
+    ref = _gpu_run(0, n, dim=dim)
+    _repro(False)
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, n, q, dim))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        got = res[r]
+        assert (got["iters"], got["freeze"], got["step_iters"], got["charges"]) == \
+            (ref["iters"], ref["freeze"], ref["step_iters"], ref["charges"])
+        assert got["lam"] == ref["lam"] and got["conv"] == ref["conv"]
+        assert got["err"] == ref["err"]
+        for x, y in zip(got["vecs"], ref["vecs"]):
+            assert np.array_equal(x, y)
 
 
 def _gpu_kiops_run(n, comm=None, dim=2):
