@@ -102,6 +102,12 @@ int64_t ek_grid_len(const ek_grid* g);
 #define EK_PART_SLOTS 8
 #define EK_PART_COUNT 5
 #define EK_PART_TAG 6
+/* part[] of the Arnoldi control block: four channels of EK_XSLOTS slots (the
+ * window dots of pass A; channel 0 alone for the sums of squares of passes B
+ * and C and of the init pass), then the non-finite count and the tag. */
+#define EK_ARN_PART_SLOTS 24
+#define EK_ARN_PART_COUNT 20
+#define EK_ARN_PART_TAG 21
 /* Returns the previous setting; negative only queries. */
 int ek_set_repro(int on);
 /* The fp64 value of a merged accumulator: `slots` = [n][EK_XSLOTS] integer
@@ -192,7 +198,8 @@ typedef struct ek_arnoldi_state {
     uint32_t ticket;    /* internal (keep 0)                                */
     int32_t defer;      /* slab mode: passes leave local sums in part[] and
                            ek_arnoldi_slab_decide applies the gathered ones  */
-    double part[6];     /* local window dots / sums of squares (slab mode)   */
+    double part[24];    /* EK_ARN_PART_SLOTS: local window dots / sums of
+                           squares (slab mode)                               */
 } ek_arnoldi_state;
 
 /* ------------------------------------------------------------ utilities */
@@ -429,7 +436,7 @@ int ek_arnoldi_run(const ek_grid* g, int jac, const double* u,
  * followed by the p tail values, replicated on every rank. The state block
  * has defer = 1: every pass leaves its LOCAL sums in st->part (n-part only:
  * tails are added once, in the decision) and ek_arnoldi_slab_decide applies
- * the rank-ordered sums of the gathered [nranks][6] part arrays:
+ * the global sums of the gathered [nranks][EK_ARN_PART_SLOTS] part blocks:
  *   which 3 after ek_arnoldi_slab_init: beta = ||V[0]||;
  *   which 0 after pass A (phase 0: Jv of V[jj-1] with the halo rows in
  *           `halo`, augmentation, window dots): H[lo.., jj-1] (+ tail dots),

@@ -75,7 +75,7 @@ class ArnoldiState(C.Structure):
                 ("tol", C.c_double), ("beta", C.c_double), ("j", C.c_int32),
                 ("happy", C.c_int32), ("status", C.c_int32),
                 ("fd_evals", C.c_int32), ("ticket", C.c_uint32),
-                ("defer", C.c_int32), ("part", C.c_double * 6)]
+                ("defer", C.c_int32), ("part", C.c_double * 24)]
 
 
 _P = C.c_void_p

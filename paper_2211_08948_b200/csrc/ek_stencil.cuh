@@ -65,6 +65,14 @@ __host__ __device__ constexpr int ep_nq(int ep) {
 // accumulators of a pass; the FD remainder also counts non-finite FD
 // Jacobian actions (the reference raises 'non-finite Jacobian action' from
 // fd_jacobian_apply before the remainder check, linalg.py:127-128)
+// Sum channels (the first ones of the epilogue's reduction) that repro mode
+// accumulates in integers (ek_xsum.cuh): ||y||^2 of the Leja / power / RHS
+// norm passes, the four window dots of the Arnoldi pass.
+__host__ __device__ constexpr int ep_nx(int ep) { return ep == EP_ARN ? 4 : 1; }
+__host__ __device__ constexpr bool ep_xsum(int ep) {
+    return ep == EP_LEJA || ep == EP_POWER || ep == EP_RHSN || ep == EP_ARN;
+}
+
 template <int EV, int EP>
 __host__ __device__ constexpr int nq_of() {
     return (EP == EP_REM && EV == EV_REMFD) ? 2 : (ep_nq(EP) > 0 ? ep_nq(EP) : 1);
@@ -629,7 +637,10 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             st_stream(a.out + e, w, ctl.wpol);
 #pragma unroll
             for (int q = 0; q < (K < 4 ? K : 4); ++q)
-                if (q < a.nwin) acc[q] += z.p[q][c] * w;
+                if (q < a.nwin) {
+                    if (ctl.repro) xadd<true>(xs[q], z.p[q][c] * w);
+                    else acc[q] += z.p[q][c] * w;
+                }
             if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
         } else {  // EP_REM
             const double r = ctl.y_zero ? 0.0 : v;  // zero direction (device-side test)
@@ -654,7 +665,7 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
 // Last-block bookkeeping of one fused pass. `xt`: the order-independent
 // total of the sum channel (repro mode; tot[0] already holds its value).
 template <int EV, int EP>
-__device__ void finalize(const KArgs& a, const double* tot, const XAcc& xt);
+__device__ void finalize(const KArgs& a, const double* tot, const XAcc* xt);
 
 template <int EP>
 __device__ __forceinline__ uint32_t* ticket_of(const KArgs& a) {
@@ -664,22 +675,18 @@ __device__ __forceinline__ uint32_t* ticket_of(const KArgs& a) {
     else return &((ek_scalar_state*)a.st)->ticket;
 }
 
-// Epilogues whose channel 0 is a sum of squares that repro mode takes over.
-__host__ __device__ constexpr bool ep_xsum(int ep) {
-    return ep == EP_LEJA || ep == EP_POWER || ep == EP_RHSN;
-}
-
 template <int EV, int EP, int NQ, int NT = TPB>
 __device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc)[NQ],
-                                                    XAcc (&xs)[1]) {
+                                                    XAcc (&xs)[ep_nx(EP)]) {
     if constexpr (ep_nq(EP) > 0) {
         // peer mode: this block's halo stores must reach the peers before
         // the last block raises the pass flag (system-scope fence)
         double tot[NQ];
-        XAcc xt[1];
-        if (reduce_grid<NQ, 1, NT>(acc, xs, ep_xsum(EP) && a.repro != 0, a.work, ticket_of<EP>(a),
-                                   a.peer != nullptr, tot, xt)) {
-            if (flat_tid() == 0) finalize<EV, EP>(a, tot, xt[0]);
+        constexpr int NX = ep_nx(EP);
+        XAcc xt[NX];
+        if (reduce_grid<NQ, NX, NT>(acc, xs, ep_xsum(EP) && a.repro != 0, a.work,
+                                    ticket_of<EP>(a), a.peer != nullptr, tot, xt)) {
+            if (flat_tid() == 0) finalize<EV, EP>(a, tot, xt);
         }
     }
 }
@@ -698,8 +705,9 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
     const long tile_rows = 8L * RPT;
     const long ntiles = tiles_c * ((rows + tile_rows - 1) / tile_rows);
     double acc[NQ];
-    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
-    xzero(xs[0]);
+    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+#pragma unroll
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -787,8 +795,9 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
     const long tk = (n + 31) / 32, tj = (n + 7) / 8, ti = (rows + RPT - 1) / RPT;
     const long ntiles = tk * tj * ti;
     double acc[NQ];
-    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
-    xzero(xs[0]);
+    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+#pragma unroll
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -881,10 +890,10 @@ __device__ __forceinline__ void part_store(double* part, const KArgs& a, double 
 }
 
 template <int EV, int EP>
-__device__ void finalize(const KArgs& a, const double* tot, const XAcc& xt) {
+__device__ void finalize(const KArgs& a, const double* tot, const XAcc* xt) {
     if constexpr (EP == EP_RHSN) {
         ek_scalar_state* st = (ek_scalar_state*)a.st;
-        if (a.repro) xstore((long long*)st->xs, xt);
+        if (a.repro) xstore((long long*)st->xs, xt[0]);
         st->repro = a.repro;
         st->val[0] = tot[0];
         st->val[1] = sqrt(tot[0]);
@@ -900,7 +909,7 @@ __device__ void finalize(const KArgs& a, const double* tot, const XAcc& xt) {
             for (int r = 0; r < P->world; ++r) {
                 double* red = (double*)((char*)P->win[r] + 64) +
                               (par * 8 + P->rank) * EK_PART_SLOTS;
-                part_store(red, a, tot[0], xt, tot[1]);
+                part_store(red, a, tot[0], xt[0], tot[1]);
             }
             __threadfence_system();
             for (int r = 0; r < P->world; ++r) {
@@ -912,14 +921,14 @@ __device__ void finalize(const KArgs& a, const double* tot, const XAcc& xt) {
             return;
         }
         if (st->defer) {  // slab mode: ek_leja_decide finishes with global sums
-            part_store(st->part, a, tot[0], xt, tot[1]);
+            part_store(st->part, a, tot[0], xt[0], tot[1]);
             return;
         }
         leja_decide(st, a.coef, a.mi, a.m, a.nk, tot[0], tot[1], EV == EV_FD);
     } else if constexpr (EP == EP_POWER) {
         ek_power_state* st = (ek_power_state*)a.st;
         if (st->defer) {
-            part_store(st->part, a, tot[0], xt, tot[1]);
+            part_store(st->part, a, tot[0], xt[0], tot[1]);
             return;
         }
         power_decide(st, tot[0], tot[1], EV == EV_FD);
@@ -927,7 +936,14 @@ __device__ void finalize(const KArgs& a, const double* tot, const XAcc& xt) {
         ek_arnoldi_state* st = (ek_arnoldi_state*)a.st;
         if (EV == EV_FD && st->nvn != 0.0) st->fd_evals += 1;
         if (st->defer) {  // slab mode: local sums; ek_arnoldi_slab_decide finishes
-            for (int q = 0; q < 5; ++q) st->part[q] = tot[q];
+            // window dots (EK_ARN_PART_*): fp64 values, or in repro mode the
+            // integer accumulators; then the non-finite count and the tag
+            for (int q = 0; q < 4; ++q) {
+                if (a.repro) xstore(reinterpret_cast<long long*>(st->part) + q * XSLOTS, xt[q]);
+                else st->part[q * XSLOTS] = tot[q];
+            }
+            st->part[EK_ARN_PART_COUNT] = tot[4];
+            st->part[EK_ARN_PART_TAG] = a.repro ? 1.0 : 0.0;
             const long n = a.g.ncomp * a.npts;
             const int p = (int)a.n_aug;
             const double* prev = a.win[a.nwin - 1];

@@ -321,8 +321,9 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
     __syncthreads();
 
     double acc[NQ];
-    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
-    xzero(xs[0]);
+    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+#pragma unroll
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 

@@ -310,8 +310,9 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
     __syncthreads();
 
     double acc[NQ];
-    XAcc xs[1];  // repro mode: the sum channel, order-independent (ek_xsum.cuh)
-    xzero(xs[0]);
+    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+#pragma unroll
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 

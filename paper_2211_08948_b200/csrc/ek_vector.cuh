@@ -435,11 +435,24 @@ struct ArnVArgs {
     const double* src;    // init: V[0][:n] source
     ek_arnoldi_state* st;
     double* work;
+    int repro;            // order-independent sums (ek_xsum.cuh)
 };
+
+// Slab mode: channel 0 of part[] (EK_ARN_PART_*) from a vector pass.
+__device__ __forceinline__ void arn_part_store(double* part, int repro, double ssq,
+                                               const XAcc& xt) {
+    if (repro) xstore(reinterpret_cast<long long*>(part), xt);
+    else part[0] = ssq;
+    part[EK_ARN_PART_COUNT] = 0.0;
+    part[EK_ARN_PART_TAG] = repro ? 1.0 : 0.0;
+}
 
 // V[0] = [w_l ; tail], beta = ||V[0]||  (kiops.py:168-176)
 __global__ void __launch_bounds__(TPB) k_arn_init(const ArnVArgs a) {
     double acc[1] = {0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
+    const bool rp = a.repro && a.st->defer;  // repro sums on the slab path
     const bool vec = al16d(a.src) && al16d(a.w);
     EK_FOR4(e0, a.n) {
         const bool full = vec && e0 + 4 <= a.n;
@@ -447,17 +460,19 @@ __global__ void __launch_bounds__(TPB) k_arn_init(const ArnVArgs a) {
         ld4(a.src, e0, a.n, full, v);
         st4(a.w, e0, a.n, full, v);
 #pragma unroll
-        for (int w = 0; w < 4; ++w) acc[0] += v[w] * v[w];  // zeros past n
+        for (int w = 0; w < 4; ++w) {  // zeros past n
+            if (rp) xadd<false>(xs[0], v[w] * v[w]);
+            else acc[0] += v[w] * v[w];
+        }
     }
-    block_sum<1>(acc);
-    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
-        double tot[1];
-        gather_partials<1>(a.work, gridDim.x, tot);
+    double tot[1];
+    XAcc xt[1];
+    if (reduce_grid<1, 1>(acc, xs, rp, a.work, &a.st->ticket, false, tot, xt)) {
         if (threadIdx.x == 0) {
             double ssq = tot[0];
             if (a.st->defer) {  // slab: beta from the gathered sums (which 3)
                 for (int t = 0; t < a.p; ++t) a.w[a.n + t] = a.tail0[t];
-                a.st->part[0] = tot[0];
+                arn_part_store(a.st->part, rp, tot[0], xt[0]);
                 a.st->happy = 0;
                 a.st->status = EK_ST_OK;
                 a.st->j = 0;
@@ -529,7 +544,10 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
     for (int q = 0; q < 4; ++q) h[q] = q < a.nwin ? a.H[(long)(lo + q) * a.ldh + (a.jj - 1)] : 0.0;
     const int64_t len = a.n + a.p;
     const bool nonly = cst->defer != 0;  // slab: the tail is added once, in the decision
+    const bool rp = a.repro && nonly;
     double acc[1] = {0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
     bool vec = al16d(a.w);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -552,18 +570,20 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             wv[w] = wv[w] - t[w];
-            if (!nonly || e0 + w < a.n) acc[0] += wv[w] * wv[w];  // zeros past len
+            if (!nonly || e0 + w < a.n) {  // zeros past len
+                if (rp) xadd<false>(xs[0], wv[w] * wv[w]);
+                else acc[0] += wv[w] * wv[w];
+            }
         }
         st4(a.w, e0, len, full, wv);
     }
-    block_sum<1>(acc);
-    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
-        double tot[1];
-        gather_partials<1>(a.work, gridDim.x, tot);
+    double tot[1];
+    XAcc xt[1];
+    if (reduce_grid<1, 1>(acc, xs, rp, a.work, &a.st->ticket, false, tot, xt)) {
         if (threadIdx.x == 0) {
             ek_arnoldi_state* st = a.st;
             if (st->defer) {
-                st->part[0] = tot[0];
+                arn_part_store(st->part, rp, tot[0], xt[0]);
                 return;
             }
             const double nrm = sqrt(tot[0]);
@@ -584,7 +604,10 @@ __global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
     if (cst->happy || cst->status) return;
     const Dv nrm = mkdv(cst->nrm);
     const int64_t len = a.n + a.p;
+    const bool rp = a.repro && cst->defer != 0;
     double acc[1] = {0.0};
+    XAcc xs[1];
+    xzero(xs[0]);
     const bool vec = al16d(a.w);
     EK_FOR4(e0, len) {
         const bool full = vec && e0 + 4 <= len;
@@ -593,16 +616,18 @@ __global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             v[w] = dv(v[w], nrm);
-            if (e0 + w < a.n) acc[0] += v[w] * v[w];
+            if (e0 + w < a.n) {
+                if (rp) xadd<false>(xs[0], v[w] * v[w]);
+                else acc[0] += v[w] * v[w];
+            }
         }
         st4(a.w, e0, len, full, v);
     }
-    block_sum<1>(acc);
-    if (publish_and_arrive<1>(acc, a.work, &a.st->ticket)) {
-        double tot[1];
-        gather_partials<1>(a.work, gridDim.x, tot);
+    double tot[1];
+    XAcc xt[1];
+    if (reduce_grid<1, 1>(acc, xs, rp, a.work, &a.st->ticket, false, tot, xt)) {
         if (threadIdx.x == 0) {
-            if (a.st->defer) a.st->part[0] = tot[0];
+            if (a.st->defer) arn_part_store(a.st->part, rp, tot[0], xt[0]);
             else a.st->nvn = sqrt(tot[0]);
             a.st->j = a.jj;
         }
@@ -610,13 +635,30 @@ __global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
 }
 
 // Slab mode: the decision of one Arnoldi pass from the gathered per-rank
-// part[6] arrays (rank order; tails, replicated on every rank, added once).
+// part[] blocks (EK_ARN_PART_*; tails, replicated on every rank, added once).
 __global__ void k_arn_decide(const ArnVArgs a, const double* g, int nranks, int which) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     ek_arnoldi_state* st = a.st;
+    // channel q of the gathered part[] blocks (EK_ARN_PART_*): the exact
+    // merge of the ranks' integer accumulators (repro mode: the same bits
+    // for every P), else the rank-ordered fp64 sum
+    const bool xs = g[EK_ARN_PART_TAG] != 0.0;
     auto sum = [&](int q) {
-        double s = g[q];
-        for (int r = 1; r < nranks; ++r) s = s + g[6 * r + q];
+        if (xs) {
+            XAcc tot;
+            xzero(tot);
+            for (int r = 0; r < nranks; ++r)
+                xmerge(tot, xload(reinterpret_cast<const long long*>(
+                                g + (long)r * EK_ARN_PART_SLOTS + q * XSLOTS)));
+            return xvalue(tot);
+        }
+        double s = g[q * XSLOTS];
+        for (int r = 1; r < nranks; ++r) s = s + g[(long)r * EK_ARN_PART_SLOTS + q * XSLOTS];
+        return s;
+    };
+    auto count = [&]() {
+        double s = 0.0;
+        for (int r = 0; r < nranks; ++r) s += g[(long)r * EK_ARN_PART_SLOTS + EK_ARN_PART_COUNT];
         return s;
     };
     const int64_t n = a.n;
@@ -629,7 +671,7 @@ __global__ void k_arn_decide(const ArnVArgs a, const double* g, int nranks, int 
     }
     if (st->happy || st->status) return;
     if (which == 0) {  // after pass A: H column (kiops.py:187) + non-finite Jv
-        if (sum(4) > 0.0) {
+        if (count() > 0.0) {
             st->status = EK_ST_JV_NONFINITE;
             return;
         }

@@ -686,6 +686,7 @@ int ek_arnoldi_init(int64_t n, int p, const double* src, const double* tail_host
         return EK_ERR_INVALID;
     }
     ArnVArgs a{};
+    a.repro = g_repro;
     a.n = n; a.p = p; a.src = src; a.w = V0; a.st = st; a.work = work;
     for (int t = 0; t < p; ++t) a.tail0[t] = tail_host[t];
     cudaStream_t s = (cudaStream_t)stream;
@@ -725,6 +726,7 @@ int ek_arnoldi_run(const ek_grid* g, int jac, const double* u, const double* fu,
         a.aug_tail[t] = aug_tail[t];
     }
     ArnVArgs b{};
+    b.repro = g_repro;
     b.n = n; b.p = p; b.H = H; b.ldh = ldh; b.st = st; b.work = work;
     for (int jj = j_begin + 1; jj <= j_end; ++jj) {
         ArnVArgs w{};
@@ -755,6 +757,7 @@ int ek_arnoldi_slab_init(int64_t n, int p, const double* src, const double* tail
         return EK_ERR_INVALID;
     }
     ArnVArgs a{};
+    a.repro = g_repro;
     a.n = n; a.p = p; a.src = src; a.w = V0; a.st = st; a.work = work;
     for (int t = 0; t < p; ++t) a.tail0[t] = tail_host[t];
     k_arn_init<<<vgrid4(n), TPB, 0, (cudaStream_t)stream>>>(a);
@@ -777,6 +780,7 @@ int ek_arnoldi_slab_pass(const ek_grid* g, int jac, const double* u, const doubl
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = ek_grid_len(g);
     ArnVArgs b{};
+    b.repro = g_repro;
     b.n = n; b.p = p; b.H = H; b.ldh = ldh; b.st = st; b.work = work; b.jj = jj;
     if (jj > 0) arn_window(b, V, jj, iop);
     b.w = V[jj];
@@ -816,6 +820,7 @@ int ek_arnoldi_slab_decide(double* const* V, int64_t n, int p, int jj, int iop, 
         return EK_ERR_INVALID;
     }
     ArnVArgs b{};
+    b.repro = g_repro;
     b.n = n; b.p = p; b.H = H; b.ldh = ldh; b.st = st; b.jj = jj;
     if (jj > 0) arn_window(b, V, jj, iop);
     b.w = V[jj];
@@ -833,6 +838,7 @@ int ek_arnoldi_augment(int64_t n, int p, const double* jv, double* const* V, int
         return EK_ERR_INVALID;
     }
     ArnVArgs a{};
+    a.repro = g_repro;
     a.n = n; a.p = p; a.jv = jv; a.H = H; a.ldh = ldh; a.st = st; a.work = work; a.jj = jj;
     a.naug = naug; a.aug_scale = aug_scale;
     for (int t = 0; t < naug; ++t) {
@@ -849,6 +855,7 @@ int ek_arnoldi_augment(int64_t n, int p, const double* jv, double* const* V, int
 int ek_arnoldi_orth(int64_t n, int p, double* const* V, int jj, int iop, double* H, int ldh,
                     ek_arnoldi_state* st, double* work, void* stream) {
     ArnVArgs a{};
+    a.repro = g_repro;
     a.n = n; a.p = p; a.H = H; a.ldh = ldh; a.st = st; a.work = work; a.jj = jj;
     arn_window(a, V, jj, iop);
     a.w = V[jj];

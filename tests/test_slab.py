@@ -324,3 +324,31 @@ def test_kiops_two_ranks_match_single_gpu(dim, n):
             assert np.linalg.norm(x - y) <= 1e-7 * np.linalg.norm(y)
     for x, y in zip(res[0]["vecs"], res[1]["vecs"]):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,n", [(2, 128), (3, 34)])
+def test_kiops_two_ranks_bitwise_equal_one_rank_slab_path(dim, n):
+    """SURVEY.md §8(e) e4 for KIOPS: with the order-independent sums (window
+    dots, ||w||, ||V[j,:n]||, beta) the slab path gives the same bits on one
+    rank and on two — Hessenberg entries, adaptive decisions, outputs."""
+    from paper_2211_08948_b200 import _device as D
+    try:
+        ref = _gpu_kiops_run(n, comm=S.SlabComm(), dim=dim)
+    finally:
+        D.COMM = None
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_kiops_worker, args=(r, world, port, n, q, dim))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert res[r]["counts"] == ref["counts"]
+        for x, y in zip(res[r]["vecs"], ref["vecs"]):
+            assert np.array_equal(x, y)
