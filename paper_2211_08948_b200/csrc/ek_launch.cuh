@@ -259,8 +259,20 @@ inline bool build_maps(const KArgs& a, TmaMaps& m) {
     return true;
 }
 
+// RP = 1: the kernel instances that accumulate the sum channels in integers
+// (repro mode, ek_xsum.cuh); RP = 0: the default instances (no trace of it).
+template <class P, int EV, int EP, int K, int RP>
+inline int launch_k_rp(const KArgs& a, cudaStream_t s);
+
 template <class P, int EV, int EP, int K>
 inline int launch_k(const KArgs& a, cudaStream_t s) {
+    if constexpr (ep_xsum(EP))
+        if (a.repro) return launch_k_rp<P, EV, EP, K, 1>(a, s);
+    return launch_k_rp<P, EV, EP, K, 0>(a, s);
+}
+
+template <class P, int EV, int EP, int K, int RP>
+inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
     constexpr int RPT = rpt_for(P::NC, ev_nch(EV), P::DIM);
     static int occ = 0;  // one per template instantiation
     if constexpr (P::DIM == 2) {
@@ -280,7 +292,7 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
             constexpr int S = tma_stages2<EV, EP, P::NC, K>();
             constexpr int SMEM = S * stage2_doubles<EV, EP, P::NC, K>() * 8;
             static int tocc = 0;
-            auto kern = k_march2d<P, EV, EP, K, S>;
+            auto kern = k_march2d<P, EV, EP, K, S, RP>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT2, SMEM) !=
@@ -303,7 +315,7 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
             constexpr int S = tma_stages<EV, EP, P::NC, K>();
             constexpr int SMEM = S * stage_doubles<EV, EP, P::NC, K>() * 8;
             static int tocc = 0;
-            auto kern = k_tma2d<P, EV, EP, K, S>;
+            auto kern = k_tma2d<P, EV, EP, K, S, RP>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, TPB, SMEM) !=
@@ -326,7 +338,7 @@ inline int launch_k(const KArgs& a, cudaStream_t s) {
         if constexpr (S >= 5) if (g_tma_mode != 0 && tma_ok(a) && build_maps<EV, EP, P::NC, K>(a, maps)) {
             constexpr int SMEM = S * stage3_doubles<EV, EP, P::NC, K>() * 8;
             static int tocc = 0;
-            auto kern = k_tma3d<P, EV, EP, K, S>;
+            auto kern = k_tma3d<P, EV, EP, K, S, RP>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT3, SMEM) !=

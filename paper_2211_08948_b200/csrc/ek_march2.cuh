@@ -146,10 +146,10 @@ __device__ __forceinline__ void issue_row(const KArgs& a, double* buf, uint64_t*
 
 // Point (i, j) from the row stages pm (i-1), pc (i), pp (i+1); t = column
 // offset inside the strip; raw slot element t + 2 is column j.
-template <class P, int EV, int EP, int K>
+template <class P, int EV, int EP, int K, class XS>
 __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                              const double* pc, const double* pp, long i, int j,
-                                             int t, int cols, double* acc, XAcc* xs) {
+                                             int t, int cols, double* acc, XS xs) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     Nb nb[NC][NCH];
@@ -202,7 +202,7 @@ __host__ __device__ __forceinline__ int march2_segs(long G, int ns) {
     return G >= ns ? (int)(G / ns) : 1;
 }
 
-template <class P, int EV, int EP, int K, int S>
+template <class P, int EV, int EP, int K, int S, int RP>
 __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
     static_assert(S >= 4, "row ring needs i-1, i, i+1 and one in flight");
     constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
@@ -257,9 +257,10 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
     __syncthreads();
 
     double acc[NQ];
-    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+    XAcc xsa[ep_nx(EP)];  // repro mode (RP = 1): the sum channels (ek_xsum.cuh)
 #pragma unroll
-    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xsa[q]);
+    const XsT<RP> xs{xsa};
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
             }
         }
         __syncwarp();
-        reduce_and_finalize<EV, EP, NQ, NT2>(a, acc, xs);
+        reduce_and_finalize<EV, EP, NQ, NT2, RP>(a, acc, xsa);
         return;
     }
 #endif
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
         release(q0 + it.L + 1, it, it.L + 1);
         q0 += it.L + 2;
     }
-    reduce_and_finalize<EV, EP, NQ, NT2>(a, acc, xs);
+    reduce_and_finalize<EV, EP, NQ, NT2, RP>(a, acc, xsa);
 }
 
 }  // namespace ek

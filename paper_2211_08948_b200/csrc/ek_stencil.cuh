@@ -582,11 +582,27 @@ __device__ __forceinline__ void st_stream(double* p, double v, uint64_t pol) {
                  : "memory");
 }
 
+// The repro-mode accumulators of a thread, with the mode in the type: RP = 0
+// the kernel instance never uses them (the default, fp64 partial sums: no
+// branch and no registers), 1 always (the instance launched in repro mode),
+// 2 decided at run time by ctl.repro (the register-staged fallback kernels).
+template <int RP>
+struct XsT {
+    static constexpr int mode = RP;
+    XAcc* p;
+};
+template <class XS>
+__device__ __forceinline__ bool xs_on(const XS&, const Ctl& ctl) {
+    if constexpr (XS::mode == 0) return false;
+    else if constexpr (XS::mode == 1) return true;
+    else return ctl.repro;
+}
+
 // Per-point epilogue; acc[] collects this thread's partial reductions.
-template <int EV, int EP, int NC, int K>
+template <int EV, int EP, int NC, int K, class XS>
 __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long off,
                                          const double (&val)[NC],
-                                         const Centre<EV, EP, NC, K>& z, double* acc, XAcc* xs) {
+                                         const Centre<EV, EP, NC, K>& z, double* acc, XS xs) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         const long e = c * a.npts + off;
@@ -596,7 +612,7 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
         } else if constexpr (EP == EP_RHSN) {
             st_stream(a.out + e, v, ctl.wpol);
             const double uc = z.y[c];
-            if (ctl.repro) xadd<false>(xs[0], uc * uc);
+            if (xs_on(xs, ctl)) xadd<false>(xs.p[0], uc * uc);
             else acc[0] += uc * uc;
             acc[1] += uc != 0.0 ? 1.0 : 0.0;
             acc[2] += isfinite(uc) ? 0.0 : 1.0;
@@ -605,7 +621,7 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             const double yn = dv(v, a.gamma) - (ctl.shift * z.y[c]);
             st_stream(a.out + e, yn, ctl.wpol);
             if (ctl.rowlen) peer_halo_store(a, ctl, off, c, yn);
-            if (ctl.repro) xadd<false>(xs[0], yn * yn);
+            if (xs_on(xs, ctl)) xadd<false>(xs.p[0], yn * yn);
             else acc[0] += yn * yn;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
 #pragma unroll
@@ -623,7 +639,7 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
             }
         } else if constexpr (EP == EP_POWER) {
             st_stream(a.out + e, v, ctl.wpol);
-            if (ctl.repro) xadd<false>(xs[0], v * v);
+            if (xs_on(xs, ctl)) xadd<false>(xs.p[0], v * v);
             else acc[0] += v * v;
             if constexpr (EV == EV_FD) acc[1] += isfinite(v) ? 0.0 : 1.0;
         } else if constexpr (EP == EP_ARN) {
@@ -638,7 +654,7 @@ __device__ __forceinline__ void epilogue(const KArgs& a, const Ctl& ctl, long of
 #pragma unroll
             for (int q = 0; q < (K < 4 ? K : 4); ++q)
                 if (q < a.nwin) {
-                    if (ctl.repro) xadd<true>(xs[q], z.p[q][c] * w);
+                    if (xs_on(xs, ctl)) xadd<true>(xs.p[q], z.p[q][c] * w);
                     else acc[q] += z.p[q][c] * w;
                 }
             if constexpr (EV == EV_FD) acc[4] += isfinite(v) ? 0.0 : 1.0;
@@ -675,7 +691,7 @@ __device__ __forceinline__ uint32_t* ticket_of(const KArgs& a) {
     else return &((ek_scalar_state*)a.st)->ticket;
 }
 
-template <int EV, int EP, int NQ, int NT = TPB>
+template <int EV, int EP, int NQ, int NT = TPB, int RP = 2>
 __device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc)[NQ],
                                                     XAcc (&xs)[ep_nx(EP)]) {
     if constexpr (ep_nq(EP) > 0) {
@@ -684,8 +700,9 @@ __device__ __forceinline__ void reduce_and_finalize(const KArgs& a, double (&acc
         double tot[NQ];
         constexpr int NX = ep_nx(EP);
         XAcc xt[NX];
-        if (reduce_grid<NQ, NX, NT>(acc, xs, ep_xsum(EP) && a.repro != 0, a.work,
-                                    ticket_of<EP>(a), a.peer != nullptr, tot, xt)) {
+        const bool repro = RP == 1 || (RP == 2 && ep_xsum(EP) && a.repro != 0);
+        if (reduce_grid<NQ, NX, NT>(acc, xs, repro, a.work, ticket_of<EP>(a),
+                                    a.peer != nullptr, tot, xt)) {
             if (flat_tid() == 0) finalize<EV, EP>(a, tot, xt);
         }
     }
@@ -705,9 +722,10 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
     const long tile_rows = 8L * RPT;
     const long ntiles = tiles_c * ((rows + tile_rows - 1) / tile_rows);
     double acc[NQ];
-    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+    XAcc xsa[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
 #pragma unroll
-    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xsa[q]);
+    const XsT<2> xs{xsa};
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -779,7 +797,7 @@ __global__ void __launch_bounds__(TPB) k_stencil2d(const KArgs a) {
             }
         }
     }
-    reduce_and_finalize<EV, EP, NQ>(a, acc, xs);
+    reduce_and_finalize<EV, EP, NQ>(a, acc, xsa);
 }
 
 // ------------------------------------------------------------ 3-D kernel
@@ -795,9 +813,10 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
     const long tk = (n + 31) / 32, tj = (n + 7) / 8, ti = (rows + RPT - 1) / RPT;
     const long ntiles = tk * tj * ti;
     double acc[NQ];
-    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+    XAcc xsa[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
 #pragma unroll
-    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xsa[q]);
+    const XsT<2> xs{xsa};
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -874,7 +893,7 @@ __global__ void __launch_bounds__(TPB) k_stencil3d(const KArgs a) {
             }
         }
     }
-    reduce_and_finalize<EV, EP, NQ>(a, acc, xs);
+    reduce_and_finalize<EV, EP, NQ>(a, acc, xsa);
 }
 
 // --------------------------------------------------------------- finalize

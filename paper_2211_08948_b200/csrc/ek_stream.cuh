@@ -189,11 +189,11 @@ __device__ __forceinline__ void issue_chunk(const TmaMaps& maps, double* buf, ui
 // One grid point (i, j) of chunk stage `raw`/`ctr`. EDGE = the chunk touches
 // the domain boundary, so ghost rows/columns may come from global memory;
 // interior chunks (the vast majority) read everything from the stage.
-template <class P, int EV, int EP, int K, bool EDGE>
+template <class P, int EV, int EP, int K, bool EDGE, class XS>
 __device__ __forceinline__ void tma_point(const KArgs& a, const Ctl& ctl, const double* raw,
                                           const double* ctr, const double* const (&rb)[2],
                                           const double* const (&rh)[2], int i, int j, int wid,
-                                          int lane, int rows, int cols, double* acc, XAcc* xs) {
+                                          int lane, int rows, int cols, double* acc, XS xs) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     const bool gx_m = EDGE && i == 0, gx_p = EDGE && i == rows - 1;  // ghost rows (warp-uniform)
@@ -271,7 +271,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // chunk k-S only if that is the oldest one still missing) and then issues as
 // many further chunks as have free stages, without waiting. Warps never
 // synchronise with each other, only with the copies they consume.
-template <class P, int EV, int EP, int K, int S>
+template <class P, int EV, int EP, int K, int S, int RP>
 __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_constant__ TmaMaps maps) {
     constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
     constexpr int NR = nraw<EV>();
@@ -321,9 +321,10 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
     __syncthreads();
 
     double acc[NQ];
-    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+    XAcc xsa[ep_nx(EP)];  // repro mode (RP = 1): the sum channels (ek_xsum.cuh)
 #pragma unroll
-    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xsa[q]);
+    const XsT<RP> xs{xsa};
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(TPB) k_tma2d(const KArgs a, const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     }
-    reduce_and_finalize<EV, EP, NQ>(a, acc, xs);
+    reduce_and_finalize<EV, EP, NQ, TPB, RP>(a, acc, xsa);
 }
 
 }  // namespace ek

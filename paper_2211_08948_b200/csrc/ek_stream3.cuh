@@ -174,11 +174,11 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
 // EDGE: bit 0 = the item touches a y edge (j = 0 / n-1), bit 1 = a z edge
 // (k = 0 / n-1); only those ghost selects are compiled in. zpar: the
 // column parity of the wrapped ghost columns -1 / n (launch constants).
-template <class P, int EV, int EP, int K, int IY, int EDGE>
+template <class P, int EV, int EP, int K, int IY, int EDGE, class XS>
 __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                            const double* pc, const double* pp,
                                            int ly, int lx, int jy, int kx, int ro, int co, int n,
-                                           long off, double* acc, XAcc* xs, int zpm, int zpp) {
+                                           long off, double* acc, XS xs, int zpm, int zpp) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     constexpr int RAW3 = raw3(IY), CTR3 = ctr3(IY);
@@ -249,7 +249,7 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
 }
 
 
-template <class P, int EV, int EP, int K, int S>
+template <class P, int EV, int EP, int K, int S, int RP>
 __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
     static_assert(S >= 4, "plane ring needs i-1, i, i+1 and one in flight");
     constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
@@ -310,9 +310,10 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
     __syncthreads();
 
     double acc[NQ];
-    XAcc xs[ep_nx(EP)];  // repro mode: the sum channels, order-independent (ek_xsum.cuh)
+    XAcc xsa[ep_nx(EP)];  // repro mode (RP = 1): the sum channels (ek_xsum.cuh)
 #pragma unroll
-    for (int q = 0; q < ep_nx(EP); ++q) xzero(xs[q]);
+    for (int q = 0; q < ep_nx(EP); ++q) xzero(xsa[q]);
+    const XsT<RP> xs{xsa};
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
 
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
             }
         }
         __syncwarp();
-        reduce_and_finalize<EV, EP, NQ, NT3>(a, acc, xs);
+        reduce_and_finalize<EV, EP, NQ, NT3, RP>(a, acc, xsa);
         return;
     }
 #endif
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
         release(q0 + it.L + 1, t, it, it.L + 1);
         q0 += it.L + 2;
     }
-    reduce_and_finalize<EV, EP, NQ, NT3>(a, acc, xs);
+    reduce_and_finalize<EV, EP, NQ, NT3, RP>(a, acc, xsa);
 }
 
 }  // namespace ek
