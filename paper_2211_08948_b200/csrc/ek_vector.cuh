@@ -823,15 +823,23 @@ __global__ void __launch_bounds__(TPB) k_vexpr(const VexprArgs a) {
                 } break;
                 case VX_STORE: a.out[arg][e] = VX_AT(sp - 1); break;
                 case VX_POP: --sp; break;
-                case VX_NORM: {
+                case VX_NORM: {  // channel 0 or 1 (static indices: registers)
                     const double t = VX_AT(sp - 1);
-                    if (a.repro) xadd<false>(xs[arg & 1], t * t);
-                    else acc[arg] += t * t;
+                    const double tt = t * t;
+                    if (a.repro) {
+                        if (arg == 0) xadd<false>(xs[0], tt);
+                        else xadd<false>(xs[1], tt);
+                    } else if (arg == 0) acc[0] += tt;
+                    else acc[1] += tt;
                 } break;
-                case VX_ACC:
-                    if (a.repro) xadd<true>(xs[arg & 1], VX_AT(sp - 1));
-                    else acc[arg] += VX_AT(sp - 1);
-                    break;
+                case VX_ACC: {
+                    const double t = VX_AT(sp - 1);
+                    if (a.repro) {
+                        if (arg == 0) xadd<true>(xs[0], t);
+                        else xadd<true>(xs[1], t);
+                    } else if (arg == 0) acc[0] += t;
+                    else acc[1] += t;
+                } break;
                 case VX_CHECK: {
                     const double t = VX_AT(sp - 1);
                     acc[2] += t != 0.0 ? 1.0 : 0.0;

@@ -131,3 +131,16 @@ def test_norm_kernels_in_repro_mode_equal_the_exact_sum():
         D.set_reproducible(old)
     nrm2, _ = D.norm2(xd)  # default mode: same value within an ulp or two
     assert abs(nrm2 - exact) <= 4e-16 * exact
+    # the general elementwise program's reductions in the default mode
+    # (linalg.dot: VX_ACC; an expression norm: VX_NORM)
+    from paper_2211_08948_b200 import linalg as LA
+    got = LA.dot(xd, yd)
+    want = math.fsum((x * y).tolist())
+    assert abs(got - want) <= 1e-12 * math.sqrt(len(x))
+    got, _ = D.evaluate([(D.V(xd) * D.V(yd), None)], xd.numel(), norm=True)
+    assert abs(got - math.sqrt(math.fsum((w * w).tolist()))) <= 1e-13 * got
+    old = D.set_reproducible(True)
+    try:
+        assert LA.dot(xd, yd) == want
+    finally:
+        D.set_reproducible(old)
