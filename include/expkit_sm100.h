@@ -305,22 +305,37 @@ int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu,
                 double gamma, ek_leja_state* st, double* work,
                 const double* const* halo, void* stream);
 
-/* One recurrence step for a Jacobian action computed elsewhere (dense,
- * callable or 1-D operators): y' = jv/gamma - shift*y, accumulators, norm,
- * freeze test (leja.py:172-184). */
+/* The same iterations as ONE launch of a CUDA graph whose WHILE node loops
+ * on the device (whole-grid path): from m_begin (1, or
+ * the even first iteration of a later 32-point chunk) until the call is done,
+ * m reaches m_limit, or the chunk's last column has been used. Every node
+ * takes its iteration index from the state block and the finalising block
+ * of an iteration sets the loop condition, so no launch ever finds the call
+ * finished and the host does nothing per iteration. Graphs are cached per
+ * kernel instance; a call rewrites the nodes' arguments. Results are those
+ * of ek_leja_run bit for bit. */
+int ek_leja_run_graph(const ek_grid* g, int jac, const double* u, const double* fu,
+                      const double* b, double* const* ybuf, double* const* p, int k,
+                      const double* coef_dev, int chunk_base, int m_begin, int m_limit,
+                      double gamma, ek_leja_state* st, double* work, void* stream);
+
 /* One whole-grid fused Leja call up to its first host check, in ONE
  * call (the single-GPU fast path of leja_interpolate_vertical,
  * leja.py:133-184): upload the first 32-point coefficient chunk from
  * `coef_host` ((k+1) x 32, as for ek_leja_run) into `coef_dev`, initialise
  * the state block (tol; ||u|| = nu, or *nu_dev when given; fold: the m = 0
  * accumulators are folded into the first iteration; lazy0 as in
- * ek_leja_state), run the begin pass, then iterations 1 .. m_end-1. */
+ * ek_leja_state), run the begin pass, then iterations 1 .. m_end-1
+ * (m_end < 0: as one graph launch, ek_leja_run_graph with m_limit = -m_end). */
 int ek_leja_call(const ek_grid* g, int jac, const double* u, const double* fu,
                  const double* b, double* const* ybuf, double* const* p, int k,
                  const double* coef_host, double* coef_dev, double tol, double nu,
                  const double* nu_dev, int fold, int lazy0, int m_end, double gamma,
                  ek_leja_state* st, double* work, void* stream);
 
+/* One recurrence step for a Jacobian action computed elsewhere (dense,
+ * callable or 1-D operators): y' = jv/gamma - shift*y, accumulators, norm,
+ * freeze test (leja.py:172-184). */
 int ek_leja_update(int64_t len, const double* jv, const double* y,
                    double* ynext, double* const* p, int k,
                    const double* coef_dev, int chunk_base, int m,

@@ -112,6 +112,8 @@ _SIGS = {
                           _I, _I, _I, _D, _P, _P, _P]),
     "ek_leja_run": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
                          _I, _I, _D, _P, _P, _PP, _P]),
+    "ek_leja_run_graph": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
+                               _I, _I, _D, _P, _P, _P]),
     "ek_leja_update": (_I, [_L, _P, _P, _P, _PP, _I, _P, _I, _I, _D, _I, _P,
                             _P, _P]),
     "ek_power_run": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _I, _I, _P, _P,

@@ -82,6 +82,32 @@ inline bool march_ok(const KArgs& a) {
 
 // 2-D staging: 0 register-staged k_stencil2d, 1 TMA 32x8 chunks (k_tma2d),
 // 2 TMA row march (k_march2d, default). 3-D: any nonzero mode = k_tma3d.
+// Launch recorder (graph mode): when set, the launchers describe the kernel
+// they would launch instead of launching it.
+struct LaunchDesc {
+    void* func;
+    dim3 grid, block;
+    size_t smem;
+    KArgs args;
+    TmaMaps maps;
+    bool has_maps;
+};
+extern thread_local LaunchDesc* g_record;
+template <typename Kern>
+inline bool record_launch(Kern kern, unsigned grid, unsigned block, size_t smem, const KArgs& a,
+                          const TmaMaps* maps) {
+    if (!g_record) return false;
+    LaunchDesc& d = *g_record;
+    d.func = (void*)kern;
+    d.grid = dim3(grid);
+    d.block = dim3(block);
+    d.smem = smem;
+    d.args = a;
+    d.has_maps = maps != nullptr;
+    if (maps) d.maps = *maps;
+    return true;
+}
+
 extern int g_tma_mode;
 extern int g_march_mask;  // auto mode: passes (bit EP_*) staged by the row march
 
@@ -295,6 +321,11 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
             auto kern = k_march2d<P, EV, EP, K, S, RP>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                // the ring is sized for two resident blocks: ask for the full
+                // shared-memory carve-out explicitly (kernel nodes of a graph
+                // do not get the direct launch's automatic choice)
+                cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT2, SMEM) !=
                         cudaSuccess || tocc < 1)
                     tocc = 1;
@@ -307,6 +338,7 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
             const unsigned grid = (unsigned)(cap >= ns ? ns * ng : cap);
             KArgs am = a;
             if (pair) { am.act_lo = 3; am.act_hi = 8; }
+            if (record_launch(kern, grid, NT2, SMEM, am, nullptr)) return EK_OK;
             kern<<<grid, NT2, SMEM, s>>>(am);
             EK_LAUNCH_CHECK("bulk-copy march stencil launch");
             if (!pair) return EK_OK;
@@ -318,6 +350,11 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
             auto kern = k_tma2d<P, EV, EP, K, S, RP>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                // the ring is sized for two resident blocks: ask for the full
+                // shared-memory carve-out explicitly (kernel nodes of a graph
+                // do not get the direct launch's automatic choice)
+                cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, TPB, SMEM) !=
                         cudaSuccess || tocc < 1)
                     tocc = 1;
@@ -327,6 +364,7 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
             const unsigned grid = (unsigned)(chunks < cap ? chunks : cap);
             KArgs ac = a;
             if (pair) { ac.act_lo = 0; ac.act_hi = 2; }
+            if (record_launch(kern, grid, TPB, SMEM, ac, &maps)) return EK_OK;
             kern<<<grid, TPB, SMEM, s>>>(ac, maps);
             EK_LAUNCH_CHECK("tma stencil launch");
             return EK_OK;
@@ -341,6 +379,11 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
             auto kern = k_tma3d<P, EV, EP, K, S, RP>;
             if (tocc == 0) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                // the ring is sized for two resident blocks: ask for the full
+                // shared-memory carve-out explicitly (kernel nodes of a graph
+                // do not get the direct launch's automatic choice)
+                cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT3, SMEM) !=
                         cudaSuccess || tocc < 1)
                     tocc = 1;
@@ -350,6 +393,7 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
                                   ((a.g.rows + SEG3 - 1) / SEG3);
             const int64_t cap = (int64_t)sm_count() * tocc;
             const unsigned grid = (unsigned)(items < cap ? items : cap);
+            if (record_launch(kern, grid, NT3, SMEM, a, &maps)) return EK_OK;
             kern<<<grid, NT3, SMEM, s>>>(a, maps);
             EK_LAUNCH_CHECK("tma3 stencil launch");
             return EK_OK;
@@ -358,9 +402,11 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
     const int64_t tiles = stencil_tiles(&a.g, RPT);
     if constexpr (P::DIM == 3) {
         auto kern = k_stencil3d<P, EV, EP, RPT, K>;
+        if (record_launch(kern, persistent_grid(kern, tiles, occ), TPB, 0, a, nullptr)) return EK_OK;
         kern<<<persistent_grid(kern, tiles, occ), TPB, 0, s>>>(a);
     } else {
         auto kern = k_stencil2d<P, EV, EP, RPT, K>;
+        if (record_launch(kern, persistent_grid(kern, tiles, occ), TPB, 0, a, nullptr)) return EK_OK;
         kern<<<persistent_grid(kern, tiles, occ), TPB, 0, s>>>(a);
     }
     EK_LAUNCH_CHECK("stencil launch");

@@ -273,6 +273,13 @@ struct KArgs {
     // reproducible sums (ek_set_repro, ek_xsum.cuh): the norm channel of the
     // reducing epilogues is accumulated in integers, independent of order
     int repro;
+    // Leja iterations as nodes of a CUDA graph WHILE loop (ek_leja_run_graph):
+    // m < 0 = take the iteration index from the state block (m = st->m + 1;
+    // -1: this node runs the odd iterations, -2: the even ones), column
+    // m - chunk_base of the coefficient table, stop before m_limit; the
+    // finalising block sets the loop condition `cond`
+    int chunk_base, m_limit, cond_on;
+    cudaGraphConditionalHandle cond;
 };
 
 // ----------------------------------------------------------------- geometry
@@ -444,6 +451,12 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
     if constexpr (EP == EP_LEJA) {
         const ek_leja_state* st = (const ek_leja_state*)a.st;
         if (st->done) return false;
+        int mi = a.mi;
+        if (a.m < 0) {  // graph loop node: the next iteration, if it is this node's turn
+            const int m = st->m + 1;
+            if ((m & 1) != (a.m & 1) || m >= a.m_limit || m - a.chunk_base >= 32) return false;
+            mi = m - a.chunk_base;
+        }
         if (a.act_hi > 0) {
             const int na = __popc(st->active);
             if (na < a.act_lo || na > a.act_hi || st->m != a.m - 1) return false;
@@ -451,11 +464,11 @@ __device__ __forceinline__ bool load_ctl(const KArgs& a, Ctl& ctl) {
         ctl.eps = st->eps;
         ctl.active = st->active;
         ctl.y_zero = (EV == EV_FD) && (st->ny == 0.0);
-        ctl.shift = a.coef[a.mi];
+        ctl.shift = a.coef[mi];
         ctl.pinit = st->p_init != 0;  // 0 only before the first iteration (m = 1, chunk 0)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            ctl.d[q] = q < a.nk ? a.coef[(1 + q) * 32 + a.mi] : 0.0;
+            ctl.d[q] = q < a.nk ? a.coef[(1 + q) * 32 + mi] : 0.0;
             ctl.d0[q] = q < a.nk ? a.coef[(1 + q) * 32] : 0.0;
         }
     } else if constexpr (EP == EP_POWER) {
@@ -943,7 +956,12 @@ __device__ void finalize(const KArgs& a, const double* tot, const XAcc* xt) {
             part_store(st->part, a, tot[0], xt[0], tot[1]);
             return;
         }
-        leja_decide(st, a.coef, a.mi, a.m, a.nk, tot[0], tot[1], EV == EV_FD);
+        const int m = a.m < 0 ? st->m + 1 : a.m;
+        const int mi = a.m < 0 ? m - a.chunk_base : a.mi;
+        leja_decide(st, a.coef, mi, m, a.nk, tot[0], tot[1], EV == EV_FD);
+        if (a.cond_on)  // another turn of the graph loop?
+            cudaGraphSetConditional(a.cond, (!st->done && m + 1 < a.m_limit &&
+                                             m + 1 - a.chunk_base < 32) ? 1u : 0u);
     } else if constexpr (EP == EP_POWER) {
         ek_power_state* st = (ek_power_state*)a.st;
         if (st->defer) {

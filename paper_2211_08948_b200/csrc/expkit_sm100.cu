@@ -7,6 +7,9 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 
 #include <cudaTypedefs.h>
@@ -35,6 +38,7 @@ static std::atomic<long long> g_launches{0};
 int g_tma_mode = 3;  // see ek_set_tma
 int g_march_mask = 1 << EP_LEJA;  // see ek_set_march
 int g_repro = 0;  // see ek_set_repro: order-independent sums (ek_xsum.cuh)
+thread_local LaunchDesc* g_record = nullptr;  // see ek_launch.cuh
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ------------------------------------------------------------- 1-D problem
@@ -471,6 +475,159 @@ int ek_leja_run(const ek_grid* g, int jac, const double* u, const double* fu, co
     return EK_OK;
 }
 
+// ------------------------------------------------- Leja loop as a CUDA graph
+// the iterations of a phi-call as a device-side loop. The
+// graph holds iteration 1 (kind A only) and a conditional WHILE node whose
+// body is two kernel nodes, the even and the odd iterations (the iterate
+// ping-pongs between two buffers, so each node's pointers are fixed); every
+// node takes its iteration index from the state block and the block that
+// finalises an iteration sets the loop condition (leja_decide: not done, and
+// the next column is still in this 32-point chunk). One graph launch runs
+// the call to its end or to the chunk boundary: no launch batch to size, no
+// launches that find the call finished, no host work per iteration.
+// Executable graphs are cached per kernel instance and launch geometry; a
+// call only rewrites the three nodes' arguments.
+namespace {
+struct LejaGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t first = nullptr, even = nullptr, odd = nullptr;
+    cudaGraphConditionalHandle cond = 0;
+};
+using LejaGraphKey = std::tuple<void*, void*, void*, unsigned, unsigned, size_t, int, int>;
+std::map<LejaGraphKey, LejaGraph> g_leja_graphs;
+std::mutex g_leja_graphs_mu;
+
+void kernel_params(const LaunchDesc& d, void** kp, cudaKernelNodeParams& p) {
+    kp[0] = (void*)&d.args;
+    kp[1] = (void*)&d.maps;
+    p = cudaKernelNodeParams{};
+    p.func = d.func;
+    p.gridDim = d.grid;
+    p.blockDim = d.block;
+    p.sharedMemBytes = (unsigned)d.smem;
+    p.kernelParams = kp;
+}
+
+int build_leja_graph(LejaGraph& lg, LaunchDesc* d, bool with_first) {
+    cudaError_t e = cudaGraphCreate(&lg.graph, 0);
+    if (e != cudaSuccess) return cuda_status(e, "leja graph: create");
+    // kind A: iteration 1 decides whether the loop runs at all (default 0);
+    // kind B (a later chunk, launched only while the call is unfinished): 1
+    e = cudaGraphConditionalHandleCreate(&lg.cond, lg.graph, with_first ? 0u : 1u,
+                                         cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) return cuda_status(e, "leja graph: conditional handle");
+    for (int i = 0; i < 3; ++i) {
+        d[i].args.cond = lg.cond;
+        d[i].args.cond_on = 1;
+    }
+    void* kp[2];
+    cudaKernelNodeParams p;
+    if (with_first) {
+        kernel_params(d[0], kp, p);
+        e = cudaGraphAddKernelNode(&lg.first, lg.graph, nullptr, 0, &p);
+        if (e != cudaSuccess) return cuda_status(e, "leja graph: first node");
+    }
+    cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+    cp.conditional.handle = lg.cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop;
+    e = cudaGraphAddNode(&loop, lg.graph, with_first ? &lg.first : nullptr, with_first ? 1 : 0,
+                         &cp);
+    if (e != cudaSuccess) return cuda_status(e, "leja graph: while node");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    kernel_params(d[1], kp, p);
+    e = cudaGraphAddKernelNode(&lg.even, body, nullptr, 0, &p);
+    if (e != cudaSuccess) return cuda_status(e, "leja graph: even node");
+    kernel_params(d[2], kp, p);
+    e = cudaGraphAddKernelNode(&lg.odd, body, &lg.even, 1, &p);
+    if (e != cudaSuccess) return cuda_status(e, "leja graph: odd node");
+    e = cudaGraphInstantiate(&lg.exec, lg.graph, 0);
+    if (e != cudaSuccess) return cuda_status(e, "leja graph: instantiate");
+    return EK_OK;
+}
+
+// Iterations m_begin .. of one chunk (until done, m_limit or the chunk end)
+// as one graph launch. m_begin == 1: the first chunk; otherwise m_begin must
+// be even (chunk boundaries are multiples of 32).
+int leja_graph_run(int ev, const KArgs& base, const double* b, double* const* ybuf,
+                   int chunk_base, int m_begin, int m_limit, cudaStream_t s) {
+    const bool with_first = m_begin == 1;
+    if (!with_first && (m_begin & 1)) {
+        set_error("leja graph: a later chunk must start at an even iteration (m=%d)", m_begin);
+        return EK_ERR_INVALID;
+    }
+    LaunchDesc d[3];
+    for (int i = 0; i < 3; ++i) {
+        KArgs a = base;
+        a.chunk_base = chunk_base;
+        a.m_limit = m_limit;
+        if (i == 0) {  // iteration 1: y_0 = b
+            a.m = 1; a.mi = 1 - chunk_base; a.y = b; a.out = ybuf[1];
+        } else if (i == 1) {  // even iterations: y_{m-1} in ybuf[1]
+            a.m = -2; a.y = ybuf[1]; a.out = ybuf[0];
+        } else {  // odd iterations > 1
+            a.m = -1; a.y = ybuf[0]; a.out = ybuf[1];
+        }
+        if (i == 0 && !with_first) continue;
+        g_record = &d[i];
+        const int rc = launch_stencil<EP_LEJA>(ev, a, s);
+        const bool recorded = g_record->func != nullptr;
+        g_record = nullptr;
+        if (rc != EK_OK) return rc;
+        if (!recorded) {
+            set_error("leja graph: launch not recorded");
+            return EK_ERR_UNSUPPORTED;
+        }
+    }
+    const LejaGraphKey key{with_first ? d[0].func : nullptr, d[1].func, d[2].func, d[1].grid.x,
+                           d[1].block.x, d[1].smem, with_first ? (int)d[0].grid.x : 0,
+                           d[1].has_maps ? 1 : 0};
+    std::lock_guard<std::mutex> lock(g_leja_graphs_mu);
+    auto it = g_leja_graphs.find(key);
+    if (it == g_leja_graphs.end()) {
+        LejaGraph lg;
+        const int rc = build_leja_graph(lg, d, with_first);
+        if (rc != EK_OK) return rc;
+        it = g_leja_graphs.emplace(key, lg).first;
+    }
+    LejaGraph& lg = it->second;
+    void* kp[2];
+    cudaKernelNodeParams p;
+    for (int i = with_first ? 0 : 1; i < 3; ++i) {
+        d[i].args.cond = lg.cond;
+        d[i].args.cond_on = 1;
+        kernel_params(d[i], kp, p);
+        cudaGraphNode_t node = i == 0 ? lg.first : (i == 1 ? lg.even : lg.odd);
+        cudaError_t e = cudaGraphExecKernelNodeSetParams(lg.exec, node, &p);
+        if (e != cudaSuccess) return cuda_status(e, "leja graph: node arguments");
+    }
+    cudaError_t e = cudaGraphLaunch(lg.exec, s);
+    if (e != cudaSuccess) return cuda_status(e, "leja graph: launch");
+    count_launch();
+    return EK_OK;
+}
+}  // namespace
+
+int ek_leja_run_graph(const ek_grid* g, int jac, const double* u, const double* fu,
+                      const double* b, double* const* ybuf, double* const* p, int k,
+                      const double* coef_dev, int chunk_base, int m_begin, int m_limit,
+                      double gamma, ek_leja_state* st, double* work, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (k < 1 || k > 8) {
+        set_error("ek_leja_run_graph: k=%d out of range", k);
+        return EK_ERR_INVALID;
+    }
+    const int ev = jv_ev(g, jac);
+    if (ev < 0) return EK_ERR_UNSUPPORTED;
+    KArgs a;
+    base_args(a, g, nullptr);
+    a.u = u; a.fu = fu; a.nk = k; a.coef = coef_dev; a.gamma = mkdv(gamma); a.st = st; a.work = work;
+    for (int q = 0; q < k; ++q) a.p[q] = p[q];
+    return leja_graph_run(ev, a, b, ybuf, chunk_base, m_begin, m_limit, (cudaStream_t)stream);
+}
+
 int ek_leja_call(const ek_grid* g, int jac, const double* u, const double* fu, const double* b,
                  double* const* ybuf, double* const* p, int k, const double* coef_host,
                  double* coef_dev, double tol, double nu, const double* nu_dev, int fold,
@@ -488,7 +645,10 @@ int ek_leja_call(const ek_grid* g, int jac, const double* u, const double* fu, c
     k_leja_init<<<1, 32, 0, s>>>(st, tol, nu, nu_dev, k, fold ? -1 : 0, lazy0);
     EK_LAUNCH_CHECK("k_leja_init");
     int rc = ek_leja_begin_len(ek_grid_len(g), b, p, k, coef_dev, st, work, stream);
-    if (rc != EK_OK || m_end <= 1) return rc;
+    if (rc != EK_OK || (m_end >= 0 && m_end <= 1)) return rc;
+    if (m_end < 0)  // graph mode: the whole first chunk as one device-side loop, up to -m_end
+        return ek_leja_run_graph(g, jac, u, fu, b, ybuf, p, k, coef_dev, 0, 1, -m_end, gamma, st,
+                                 work, stream);
     return ek_leja_run(g, jac, u, fu, b, ybuf, p, k, coef_dev, 0, 1, m_end, gamma, st, work,
                        nullptr, stream);
 }

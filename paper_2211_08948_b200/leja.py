@@ -44,6 +44,11 @@ _cached_points = None
 # with CUDA events bracketing its ek_leja_run launch batches.
 PROFILE = None
 _FASTCALL = os.environ.get("EK_LEJA_FASTCALL", "1") != "0"  # A/B switch (tools)
+# the iterations of a whole-grid fused call as ONE launch
+# of a CUDA graph with a device-side WHILE loop (ek_leja_run_graph): the call
+# runs to its end or to the 32-point chunk boundary with no launch batch to
+# size. "0" keeps the launch batches (A/B runs, tools).
+_GRAPH = [os.environ.get("EK_LEJA_GRAPH", "1") != "0"]
 
 
 def generate_leja_points(m=DEFAULT_NUM_POINTS, n_candidates=DEFAULT_CANDIDATES):
@@ -422,13 +427,17 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     # fused single-GPU path: the begin pass only takes ||b|| and the m = 0
     # decisions; the first iteration writes p_i = d_i[0] b + d_i[1] y_1
     fold = Jn is not None and not slab and max_points > 1
+    # graph mode: one graph launch covers the whole first chunk
+    graph = fold and _FASTCALL and _GRAPH[0]
+    # (speculate only when the group's previous count fits the first chunk: a
+    # call that crosses a chunk needs the host for its next table)
     spec = _spec is not None and fold and min(_CHUNK, max_points) > int(_first_batch)
     spec_zero = spec and _spec_zero and _lazy_m0 and isinstance(b, torch.Tensor)
     lazy = bool(_lazy_m0 and fold and (spec_zero or not spec) and isinstance(b, torch.Tensor))
     # whole-grid fused call without profiling: table upload, state init,
     # begin pass and the first launch batch in ONE native call
     fast = fold and PROFILE is None and _FASTCALL
-    first_hi = min(m_avail, 1 + max(1, int(_first_batch)))
+    first_hi = m_avail if graph else min(m_avail, 1 + max(1, int(_first_batch)))
     st = D.DevState(N.LejaState, upload=not fast, tol=float(tol), nu=nu, k=k,
                     defer=1 if slab else 0, p_init=-1 if fold else 0, lazy0=1 if lazy else 0)
     nu_ptr = None if nu_dev is None else \
@@ -442,7 +451,8 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()), C.c_void_p(Jn.fu.data_ptr()),
             C.c_void_p(bd.data_ptr()), N.ptrs(ybuf or []), pp, k, table.host.ctypes.data_as(C.c_void_p),
             C.c_void_p(table.dev.data_ptr()), float(tol), nu, nu_ptr, 1, 1 if lazy else 0,
-            1 if spec_zero else first_hi, float(gamma), st.ptr, ws, D.stream()), "ek_leja_call")
+            1 if spec_zero else (-first_hi if graph else first_hi), float(gamma), st.ptr, ws,
+            D.stream()), "ek_leja_call")
     else:
         table.upload()
         if nu_ptr is not None:
@@ -520,6 +530,12 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                         C.c_void_p(table.dev.data_ptr()), base, mm, mm + 1, float(gamma),
                         st.ptr, ws, Jn.halos(v=yprev), D.stream()), "ek_leja_run")
                     _slab_decide(st, Jn, table, base, mm, k, begin=False)
+            elif graph:
+                N.check(N.lib().ek_leja_run_graph(
+                    C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
+                    C.c_void_p(Jn.fu.data_ptr()), C.c_void_p(bd.data_ptr()), yp, pp, k,
+                    C.c_void_p(table.dev.data_ptr()), base, m, hi, float(gamma), st.ptr,
+                    ws, D.stream()), "ek_leja_run_graph")
             else:
                 N.check(N.lib().ek_leja_run(
                     C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
