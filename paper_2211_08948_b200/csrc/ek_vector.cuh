@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(TPB) k_arn_init(const ArnVArgs a) {
     double acc[1] = {0.0};
     XAcc xs[1];
     xzero(xs[0]);
-    const bool rp = a.repro && a.st->defer;  // repro sums on the slab path
+    const bool rp = a.repro != 0;
     const bool vec = al16d(a.src) && al16d(a.w);
     EK_FOR4(e0, a.n) {
         const bool full = vec && e0 + 4 <= a.n;
@@ -543,8 +543,11 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) h[q] = q < a.nwin ? a.H[(long)(lo + q) * a.ldh + (a.jj - 1)] : 0.0;
     const int64_t len = a.n + a.p;
-    const bool nonly = cst->defer != 0;  // slab: the tail is added once, in the decision
-    const bool rp = a.repro && nonly;
+    // slab: the tail is added once, in the decision; repro mode forms the
+    // norm the same way on the whole grid (the n-part as an order-independent
+    // sum, then the tail terms), so both give the same bits
+    const bool rp = a.repro != 0;
+    const bool nonly = cst->defer != 0 || rp;
     double acc[1] = {0.0};
     XAcc xs[1];
     xzero(xs[0]);
@@ -586,7 +589,13 @@ __global__ void __launch_bounds__(TPB) k_arn_orth(const ArnVArgs a) {
                 arn_part_store(st->part, rp, tot[0], xt[0]);
                 return;
             }
-            const double nrm = sqrt(tot[0]);
+            double ssq = tot[0];
+            if (rp)  // as k_arn_decide (which = 1): the tail, written by this pass
+                for (int t = 0; t < a.p; ++t) {
+                    const double tv = __ldcg(a.w + a.n + t);
+                    ssq += tv * tv;
+                }
+            const double nrm = sqrt(ssq);
             st->nrm = nrm;
             if (nrm < st->tol) {  // happy breakdown, kiops.py:190-192
                 st->happy = 1;
@@ -604,7 +613,7 @@ __global__ void __launch_bounds__(TPB) k_arn_scale(const ArnVArgs a) {
     if (cst->happy || cst->status) return;
     const Dv nrm = mkdv(cst->nrm);
     const int64_t len = a.n + a.p;
-    const bool rp = a.repro && cst->defer != 0;
+    const bool rp = a.repro != 0;
     double acc[1] = {0.0};
     XAcc xs[1];
     xzero(xs[0]);

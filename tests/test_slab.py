@@ -337,6 +337,14 @@ def test_kiops_two_ranks_bitwise_equal_one_rank_slab_path(dim, n):
         ref = _gpu_kiops_run(n, comm=S.SlabComm(), dim=dim)
     finally:
         D.COMM = None
+    # ... and the whole-grid fused Arnoldi passes in repro mode form the same
+    # sums (n-part as an integer accumulator, then the tail terms)
+    _repro(True)
+    whole = _gpu_kiops_run(n, dim=dim)
+    _repro(False)
+    assert whole["counts"] == ref["counts"]
+    for x, y in zip(whole["vecs"], ref["vecs"]):
+        assert np.array_equal(x, y)
     world, port = 2, _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

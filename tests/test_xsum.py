@@ -144,3 +144,44 @@ def test_norm_kernels_in_repro_mode_equal_the_exact_sum():
         assert LA.dot(xd, yd) == want
     finally:
         D.set_reproducible(old)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n,fd", [("brusselator_periodic", 96, True),
+                                       ("allen_cahn", 65, True), ("advdiff2d", 128, False)])
+def test_repro_mode_is_independent_of_the_kernel_staging(name, n, fd):
+    """The stagings of the 2-D stencil passes (register-staged, 32 x 8 TMA
+    chunks, row march) give bit-identical pointwise results and differ only in
+    how the norms' partial sums are grouped (ek_set_tma). With the
+    order-independent sums nothing is left to differ: a whole vertical Leja
+    call — FD increments and freeze decisions included — has the same bits
+    under every staging (n = 65: odd rows, the register-staged fallback)."""
+    import paper_2211_08948_b200 as ek
+    from paper_2211_08948_b200 import _device as D, ext
+    lib = _lib()
+    p = ek.make_problem(name, n=n) if name in ek.PROBLEMS else ext.make_ext_problem(name, n=n)
+    xi = ek.get_leja_points(400)
+    old_r = D.set_reproducible(True)
+    old_t = lib.ek_set_tma(-1)
+    try:
+        outs = []
+        for mode in (0, 1, 2, 3):
+            lib.ek_set_tma(mode)
+            rhs = ek.CountingRhs(p.rhs)
+            sys_ = ek.make_linearized(rhs, p.u0, jac_factory=None if fd else p.jac_factory)
+            lam, _ = ek.power_iterate(sys_.J)
+            est = ek.make_estimate(lam)
+            dt = 25.0 / abs(est.alpha)
+            r = ek.leja_interpolate_vertical(sys_.J, sys_.f_n * dt, 1, [0.5, 1.0], dt, est,
+                                             1e-10, xi=xi)
+            outs.append((lam, r))
+        lam0, r0 = outs[0]
+        assert r0.iters > 3
+        for lam, r in outs[1:]:
+            assert lam == lam0
+            assert r.iters == r0.iters and r.freeze_iters == r0.freeze_iters
+            for x, y in zip(r.vectors, r0.vectors):
+                assert np.array_equal(x, y)
+    finally:
+        lib.ek_set_tma(old_t)
+        D.set_reproducible(old_r)
