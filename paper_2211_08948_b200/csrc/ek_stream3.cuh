@@ -67,14 +67,17 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
 #endif
 constexpr int T3 = EK_T3, NW3 = T3 / 32;
 constexpr int NT3 = T3 + (EK_PROD3 ? 32 : 0);  // threads per block
-constexpr int I3X = 64;
+#ifndef EK_I3X
+#define EK_I3X 64  // item width along the contiguous axis (A/B: 128)
+#endif
+constexpr int I3X = EK_I3X;
 constexpr int TBW3 = I3X + 4;
 __host__ __device__ constexpr int raw3(int iy) { return (TBW3 * (iy + 2) + 15) / 16 * 16; }
 __host__ __device__ constexpr int ctr3(int iy) { return I3X * iy; }
 // Ghost side slots of a raw field (boundary items only): the wrapped /
 // reflected row above (j = -1) and below (j = n), TBW3 wide, and the ghost
 // column pair left (k = -1) and right (k = n), IY + 2 rows; 128-B multiples.
-constexpr int GROW3 = 80;  // >= TBW3
+constexpr int GROW3 = (TBW3 + 15) / 16 * 16;  // >= TBW3, a 128-B multiple
 __host__ __device__ constexpr int gcol3(int iy) { return (2 * (iy + 2) + 15) / 16 * 16; }
 __host__ __device__ constexpr int side3(int iy) { return 2 * GROW3 + 2 * gcol3(iy); }
 template <int EV, int EP, int NC, int K>

@@ -28,11 +28,15 @@ def main():
                     help="2 row march (default), 1 32x8 chunks, 0 register-staged")
     ap.add_argument("--kiops", action="store_true")
     ap.add_argument("--reps", type=int, default=5, help="timed repetitions (median)")
+    ap.add_argument("--repro", action="store_true",
+                    help="order-independent sums (ek_set_repro): the RP = 1 kernel instances")
     args = ap.parse_args()
 
     import torch
     import paper_2211_08948_b200 as ek
     from paper_2211_08948_b200 import ext, leja as L, _native as NAT
+    if args.repro:
+        NAT.lib().ek_set_repro(1)
     if args.no_tma:
         NAT.lib().ek_set_tma(0)
     if args.tma_mode is not None:
@@ -75,7 +79,7 @@ def main():
     base = 4 if fd else (2 if lin else 3)
     per = 8 * n * (base + 2 * args.k)
     per_pass = per - (8 * n if fd else 0)
-    out = {"problem": args.problem, "tma_mode": args.tma_mode,
+    out = {"problem": args.problem, "tma_mode": args.tma_mode, "repro": bool(args.repro),
            "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
            "ms_per_launch": t / args.iters * 1e3, "bytes_per_launch": per,
            "GBps": per * args.iters / t / 1e9, "GBps_pass": per_pass * args.iters / t / 1e9,
