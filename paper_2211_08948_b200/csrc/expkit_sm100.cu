@@ -494,7 +494,7 @@ struct LejaGraph {
     cudaGraphNode_t first = nullptr, even = nullptr, odd = nullptr;
     cudaGraphConditionalHandle cond = 0;
 };
-using LejaGraphKey = std::tuple<void*, void*, void*, unsigned, unsigned, size_t, int, int>;
+using LejaGraphKey = std::tuple<void*, void*, void*, unsigned, unsigned, size_t, int, int, int>;
 std::map<LejaGraphKey, LejaGraph> g_leja_graphs;
 std::mutex g_leja_graphs_mu;
 
@@ -581,9 +581,11 @@ int leja_graph_run(int ev, const KArgs& base, const double* b, double* const* yb
             return EK_ERR_UNSUPPORTED;
         }
     }
+    int dev = 0;
+    cudaGetDevice(&dev);  // executable graphs belong to one device
     const LejaGraphKey key{with_first ? d[0].func : nullptr, d[1].func, d[2].func, d[1].grid.x,
                            d[1].block.x, d[1].smem, with_first ? (int)d[0].grid.x : 0,
-                           d[1].has_maps ? 1 : 0};
+                           d[1].has_maps ? 1 : 0, dev};
     std::lock_guard<std::mutex> lock(g_leja_graphs_mu);
     auto it = g_leja_graphs.find(key);
     if (it == g_leja_graphs.end()) {
