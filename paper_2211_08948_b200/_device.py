@@ -277,6 +277,22 @@ def global_sum(v):
     return v if COMM is None else COMM.allsum([float(v)])[0]
 
 
+def global_sum_state(h):
+    """val[0] of a reduced ek_scalar_state (a sum: a dot product), global in
+    slab mode — the exact merge of the ranks' integer accumulators in repro
+    mode, as `global_norm`."""
+    if COMM is None:
+        return float(h.val[0])
+    if h.repro:
+        rows = COMM.allgather_ints([int(v) for v in h.xs])
+        slots = (C.c_int64 * (N.XSLOTS * len(rows)))()
+        for r, row in enumerate(rows):
+            for i in range(N.XSLOTS):
+                slots[r * N.XSLOTS + i] = row[i]
+        return N.lib().ek_xsum_value(slots, len(rows))
+    return COMM.allsum([float(h.val[0])])[0]
+
+
 def norm2(x, st=None):
     """(||x||, flags) of a device vector; synchronises. flags bit0: any
     nonzero, bit1: any non-finite."""

@@ -289,7 +289,7 @@ def dot(x, y):
     N.check(N.lib().ek_vexpr(xd.numel(), code, len(pr.code), (C.c_double * 1)(), 0,
                              N.ptrs(pr.ins), len(pr.ins), N.ptrs([]), 0, st.ptr,
                              D.work_ptr(), D.stream()), "ek_vexpr")
-    return D.global_sum(float(st.read().val[0]))
+    return D.global_sum_state(st.read())
 
 
 def axpy(alpha, x, y):
