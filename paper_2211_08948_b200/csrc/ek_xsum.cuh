@@ -167,10 +167,10 @@ __host__ __device__ inline double xvalue(const XAcc& x) {
     unsigned long long mant = top64 >> 11;
     const unsigned long long rem = top64 & 0x7ffull;
     if (rem > 0x400ull || (rem == 0x400ull && (sticky || (mant & 1ull)))) ++mant;
-    // top64's LSB sits at absolute bit 32*(top-3) + 32*(4-h-2) + 32 - lz - ... :
-    // limb h has weight 2^(32*(4-h)) relative to the window bottom; M = limb h
-    // : limb h+1 has its LSB at 32*(3-h); top64 = M*2^lz plus lower bits, so
-    // its LSB is at 32*(3-h) - lz; mant's LSB is 11 above that.
+    // Relative to the window bottom (absolute bit 32*(top-3)) limb h has
+    // weight 2^(32*(4-h)), so M = (limb h : limb h+1) has its LSB at bit
+    // 32*(3-h), top64 = M * 2^lz (plus bits of limb h+2) at 32*(3-h) - lz, and
+    // mant = top64 >> 11 eleven bits above that; bit 0 is 2^-1074.
     const int ex = 32 * (x.top - 3) + 32 * (3 - h) - lz + 11 - 1074;
     double v = (double)(long long)mant;  // <= 2^53: exact
 #ifdef __CUDA_ARCH__
