@@ -375,6 +375,7 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
         constexpr int S = tma_stages3<EV, EP, P::NC, K>();
         if constexpr (S >= 5) if (g_tma_mode != 0 && tma_ok(a) && build_maps<EV, EP, P::NC, K>(a, maps)) {
             constexpr int SMEM = S * stage3_doubles<EV, EP, P::NC, K>() * 8;
+            constexpr int NT = nt3_of<EV, EP, P::NC, K>();  // threads per block
             static int tocc = 0;
             auto kern = k_tma3d<P, EV, EP, K, S, RP>;
             if (tocc == 0) {
@@ -384,7 +385,7 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
                 // do not get the direct launch's automatic choice)
                 cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
-                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT3, SMEM) !=
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, kern, NT, SMEM) !=
                         cudaSuccess || tocc < 1)
                     tocc = 1;
             }
@@ -393,8 +394,8 @@ inline int launch_k_rp(const KArgs& a, cudaStream_t s) {
                                   ((a.g.rows + SEG3 - 1) / SEG3);
             const int64_t cap = (int64_t)sm_count() * tocc;
             const unsigned grid = (unsigned)(items < cap ? items : cap);
-            if (record_launch(kern, grid, NT3, SMEM, a, &maps)) return EK_OK;
-            kern<<<grid, NT3, SMEM, s>>>(a, maps);
+            if (record_launch(kern, grid, NT, SMEM, a, &maps)) return EK_OK;
+            kern<<<grid, NT, SMEM, s>>>(a, maps);
             EK_LAUNCH_CHECK("tma3 stencil launch");
             return EK_OK;
         }

@@ -30,6 +30,12 @@ namespace ek {
 constexpr int W2 = 256;    // columns per strip
 constexpr int T2 = 256;    // compute threads: one column each
 constexpr int NW2 = T2 / 32;
+#ifndef EK_TIGHT2
+#define EK_TIGHT2 1  // 1: the row loop without per-row divisions (producer-warp build)
+#endif
+#ifndef EK_WAIT2_NS
+#define EK_WAIT2_NS 1000  // > 0: suspend-time hint (ns) of the row waits' try_wait
+#endif
 #ifndef EK_PROD2
 #define EK_PROD2 1  // 1: one extra producer warp issues the row copies
 #endif
@@ -287,6 +293,44 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
     }
 #endif
 
+#if EK_PROD2 && EK_TIGHT2
+    // Tight row loop (producer-warp build): the ring position is a stage
+    // index plus one phase bit per stage — every sequence number is waited
+    // for exactly once by each warp, in order — so the loop carries no
+    // division; a warp whose row has not landed sleeps in the barrier unit
+    // (try_wait with a suspend-time hint) instead of spinning.
+    int sn = 0;         // stage of the next sequence number this warp waits for
+    uint32_t ph = 0;    // bit s: parity of that wait on stage s
+    auto wait_next = [&]() {
+        const int s = sn;
+        mbar_wait_ns<EK_WAIT2_NS>(&full[s], (ph >> s) & 1u);
+        ph ^= 1u << s;
+        sn = s + 1 == S ? 0 : s + 1;
+        return s;
+    };
+    auto release_s = [&](int s) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    };
+    for (long tt = blockIdx.x; tt < nitems; tt += G) {
+        const Item2 it = item2(tt, ns, ng, rows);
+        const int j = it.j0 + t;
+        const bool live = j < cols;
+        int sm = wait_next(), sc = wait_next();
+        const double* pm = smem + sm * SD;
+        const double* pc = smem + sc * SD;
+        long i = it.r0;
+        for (int p = 1; p <= it.L; ++p, ++i) {
+            const int sp = wait_next();
+            const double* pp = smem + sp * SD;
+            if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs);
+            release_s(sm);
+            sm = sc; sc = sp; pm = pc; pc = pp;
+        }
+        release_s(sm);
+        release_s(sc);
+    }
+#else
     auto wait_full = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
     auto release = [&](int q, const Item2& it, int pos) {
         __syncwarp();
@@ -325,6 +369,7 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
         release(q0 + it.L + 1, it, it.L + 1);
         q0 += it.L + 2;
     }
+#endif
     reduce_and_finalize<EV, EP, NQ, NT2, RP>(a, acc, xsa);
 }
 

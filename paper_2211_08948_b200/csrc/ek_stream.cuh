@@ -92,6 +92,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// The same wait with a suspend-time hint of NS nanoseconds: a warp whose
+// stage has not landed sleeps in the barrier unit instead of spinning
+// through issue slots the other warps need (NS = 0: plain try_wait loop).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+template <int NS>
+__device__ __forceinline__ void mbar_wait_ns(uint64_t* bar, uint32_t parity) {
+    if constexpr (NS > 0) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n"
+            "LAB_WAITH:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+            "@!P1 bra LAB_WAITH;\n}" ::"r"(smem_u32(bar)),
+            "r"(parity), "r"(NS)
+            : "memory");
+    } else if constexpr (NS < 0) {  // A/B: back off with nanosleep between polls
+        while (!mbar_test(bar, parity)) __nanosleep(-NS);
+    } else {
+        mbar_wait(bar, parity);
+    }
+}
 
 // raw neighbourhood fields per value kind
 template <int EV>

@@ -24,6 +24,8 @@
 // the moment a stage frees up and no warp ever waits for another one.
 #pragma once
 
+#include <type_traits>
+
 #include "ek_stream.cuh"
 
 namespace ek {
@@ -65,8 +67,18 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
 #ifndef EK_PROD3
 #define EK_PROD3 1  // 1: one extra producer warp issues the plane copies
 #endif
-constexpr int T3 = EK_T3, NW3 = T3 / 32;
-constexpr int NT3 = T3 + (EK_PROD3 ? 32 : 0);  // threads per block
+#ifndef EK_TIGHT3
+#define EK_TIGHT3 1  // 1: the plane loop with hoisted per-thread geometry (producer-warp build)
+#endif
+#ifndef EK_WAIT3_NS
+#define EK_WAIT3_NS 1000  // > 0: suspend-time hint (ns) of the plane waits' try_wait
+#endif
+#ifndef EK_T3_IY8
+#define EK_T3_IY8 256  // compute threads of the IY = 8 items (two points per thread, as IY = 16)
+#endif
+#ifndef EK_CARRY3
+#define EK_CARRY3 0  // 1: single-field instances carry planes i-1 / i in registers (measured slower)
+#endif
 #ifndef EK_I3X
 #define EK_I3X 64  // item width along the contiguous axis (A/B: 128)
 #endif
@@ -94,6 +106,17 @@ __host__ __device__ constexpr int iy3() {
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage3_doubles() {
     return stage3_doubles_iy<EV, EP, NC, K>(iy3<EV, EP, NC, K>());
+}
+
+// Compute threads / threads per block of an instantiation (the producer warp
+// is one more warp).
+template <int EV, int EP, int NC, int K>
+__host__ __device__ constexpr int t3_of() {
+    return iy3<EV, EP, NC, K>() == 16 ? EK_T3 : EK_T3_IY8;
+}
+template <int EV, int EP, int NC, int K>
+__host__ __device__ constexpr int nt3_of() {
+    return t3_of<EV, EP, NC, K>() + (EK_PROD3 ? 32 : 0);
 }
 
 struct Item3 {
@@ -177,11 +200,16 @@ __device__ __forceinline__ void issue_plane(const KArgs& a, const TmaMaps& maps,
 // EDGE: bit 0 = the item touches a y edge (j = 0 / n-1), bit 1 = a z edge
 // (k = 0 / n-1); only those ghost selects are compiled in. zpar: the
 // column parity of the wrapped ghost columns -1 / n (launch constants).
-template <class P, int EV, int EP, int K, int IY, int EDGE, class XS>
+// CARRY (one raw field, one component): cv[0] / cv[1] hold the point's
+// values in planes i-1 / i from the two previous plane steps, so only plane
+// i+1's value is read from its stage (pm is not touched) and the values move
+// down one plane afterwards.
+template <class P, int EV, int EP, int K, int IY, int EDGE, class XS, bool CARRY = false>
 __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                            const double* pc, const double* pp,
                                            int ly, int lx, int jy, int kx, int ro, int co, int n,
-                                           long off, double* acc, XS xs, int zpm, int zpp) {
+                                           long off, double* acc, XS xs, int zpm, int zpp,
+                                           double* cv = nullptr) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = needs_fu<EV>() ? 1 : 0;
     constexpr int RAW3 = raw3(IY), CTR3 = ctr3(IY);
@@ -198,9 +226,16 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
         for (int f = 0; f < NR; ++f) {
             const int o = (f * NC + c) * RAW3 + ro;
             const double* bx = pc + o;
-            rc[f] = bx[0];
-            rxm[f] = pm[o];
             rxp[f] = pp[o];
+            if constexpr (CARRY) {
+                rxm[f] = cv[0];
+                rc[f] = cv[1];
+                cv[0] = rc[f];
+                cv[1] = rxp[f];
+            } else {
+                rc[f] = bx[0];
+                rxm[f] = pm[o];
+            }
             // ghost rows / columns from the side slots the copy engine filled
             const double* sd = pc + SIDE + (f * NC + c) * side3(IY);
             if constexpr (EY) {
@@ -253,11 +288,13 @@ __device__ __forceinline__ void tma3_point(const KArgs& a, const Ctl& ctl, const
 
 
 template <class P, int EV, int EP, int K, int S, int RP>
-__global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__((nt3_of<EV, EP, P::NC, K>()), EK_LB3)
+k_tma3d(const KArgs a, const __grid_constant__ TmaMaps maps) {
     static_assert(S >= 4, "plane ring needs i-1, i, i+1 and one in flight");
     constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
     constexpr int NR = nraw<EV>();
     constexpr int SD = stage3_doubles<EV, EP, NC, K>();
+    constexpr int T3 = t3_of<EV, EP, NC, K>(), NW3 = T3 / 32, NT3 = nt3_of<EV, EP, NC, K>();
     constexpr int IY = iy3<EV, EP, NC, K>(), PPT = IY * I3X / T3;
     static_assert(PPT >= 1 && PPT * T3 == IY * I3X, "item points must split evenly");
     extern __shared__ __align__(1024) double smem[];
@@ -344,6 +381,138 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
     }
 #endif
 
+    const int zpm = (int)(wrap_idx(-1, n, a.g.bc) & 1), zpp = (int)(wrap_idx(n, n, a.g.bc) & 1);
+#if EK_PROD3 && EK_TIGHT3
+    // Tight plane loop (producer-warp build). Everything that depends only
+    // on the thread is formed once: its points' (row, column) in the item,
+    // their offsets inside a raw / centre slot. The ring position is a stage
+    // index plus one phase bit per stage (every sequence number is waited
+    // for exactly once by each warp, in order), so the loop carries no
+    // division, and the item's edge class is decided outside the plane loop.
+    constexpr bool CARRY = EK_CARRY3 && NR * NC == 1;
+    int lyv[PPT], lxv[PPT], rov[PPT], cov[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r) {
+        if constexpr (IY == NW3 && PPT == 2 && !EK_MAP3_FLAT) {
+            lyv[r] = threadIdx.x >> 5;
+            lxv[r] = lane + 32 * r;
+        } else {
+            const int idx = threadIdx.x + r * T3;
+            lyv[r] = idx / I3X;
+            lxv[r] = idx % I3X;
+        }
+        rov[r] = (1 + lyv[r]) * TBW3 + 2 + lxv[r];
+        cov[r] = lyv[r] * I3X + lxv[r];
+    }
+    int sn = 0;         // stage of the next sequence number this warp waits for
+    uint32_t ph = 0;    // bit s: parity of that wait on stage s
+    auto wait_next = [&]() {
+        const int s = sn;
+        mbar_wait_ns<EK_WAIT3_NS>(&full[s], (ph >> s) & 1u);
+        ph ^= 1u << s;
+        sn = s + 1 == S ? 0 : s + 1;
+        return s;
+    };
+    auto release_s = [&](int s) {
+        // the stage's shared-memory reads of this warp have completed (their
+        // values were consumed), so no fence is needed before the copy
+        // engine may overwrite it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    };
+    const long plane = (long)n * n;
+    for (long t = blockIdx.x; t < nitems; t += G) {
+        const Item3 it = item3<IY>(t, n, rows);
+#ifdef EK_NOEDGE3  // timing experiment only: wrong results on boundary items
+        const int edge = 0;
+#else
+        const int edge = ((it.j0 < 1 || it.j0 + IY >= n) ? 1 : 0) |
+                         ((it.k0 < 1 || it.k0 + I3X >= n) ? 2 : 0);
+#endif
+        int sm = wait_next(), sc = wait_next();
+        long off[PPT];
+#pragma unroll
+        for (int r = 0; r < PPT; ++r)
+            off[r] = ((long)it.i0 * n + it.j0 + lyv[r]) * n + it.k0 + lxv[r];
+        const double* pm = smem + sm * SD;
+        const double* pc = smem + sc * SD;
+        // CARRY: planes i-1 / i of each point live in registers; the stage of
+        // plane i-1 is released before the plane loop and every stage one
+        // plane step earlier, so one more plane is in flight.
+        double cv[CARRY ? PPT : 1][2];
+        if constexpr (CARRY) {
+#pragma unroll
+            for (int r = 0; r < PPT; ++r) {
+                cv[r][0] = pm[rov[r]];
+                cv[r][1] = pc[rov[r]];
+            }
+            release_s(sm);
+        }
+        // one plane step of the item; E = -1: the edge class per point
+        auto plane_step = [&](auto etag, const double* pp) {
+            constexpr int E = decltype(etag)::value;
+#pragma unroll
+            for (int r = 0; r < PPT; ++r) {
+                double* c = CARRY ? cv[CARRY ? r : 0] : nullptr;
+                if constexpr (E == 0) {
+                    tma3_point<P, EV, EP, K, IY, 0, decltype(xs), CARRY>(
+                        a, ctl, pm, pc, pp, lyv[r], lxv[r], 0, 0, rov[r], cov[r], n, off[r], acc,
+                        xs, zpm, zpp, c);
+                } else {
+                    const int jy = it.j0 + lyv[r], kx = it.k0 + lxv[r];
+                    if (jy < n && kx < n) {
+                        // y-edge items: only the rows j = 0 / n-1 need the selects
+                        const int e = edge & ~((jy > 0 && jy < n - 1) ? 1 : 0);
+                        if (e == 2)
+                            tma3_point<P, EV, EP, K, IY, 2, decltype(xs), CARRY>(
+                                a, ctl, pm, pc, pp, lyv[r], lxv[r], jy, kx, rov[r], cov[r], n,
+                                off[r], acc, xs, zpm, zpp, c);
+                        else if (e == 0)
+                            tma3_point<P, EV, EP, K, IY, 0, decltype(xs), CARRY>(
+                                a, ctl, pm, pc, pp, lyv[r], lxv[r], jy, kx, rov[r], cov[r], n,
+                                off[r], acc, xs, zpm, zpp, c);
+                        else
+                            tma3_point<P, EV, EP, K, IY, 3, decltype(xs), CARRY>(
+                                a, ctl, pm, pc, pp, lyv[r], lxv[r], jy, kx, rov[r], cov[r], n,
+                                off[r], acc, xs, zpm, zpp, c);
+                    } else if constexpr (CARRY) {  // keep the carried planes in step
+                        c[0] = c[1];
+                        c[1] = pp[rov[r]];
+                    }
+                }
+                off[r] += plane;
+            }
+        };
+        auto advance = [&](int sp, const double* pp) {
+            if constexpr (CARRY) {
+                release_s(sc);
+            } else {
+                release_s(sm);
+                sm = sc;
+                pm = pc;
+            }
+            sc = sp;
+            pc = pp;
+        };
+        if (edge == 0) {
+            for (int p = 1; p <= it.L; ++p) {
+                const int sp = wait_next();
+                const double* pp = smem + sp * SD;
+                plane_step(std::integral_constant<int, 0>{}, pp);
+                advance(sp, pp);
+            }
+        } else {
+            for (int p = 1; p <= it.L; ++p) {
+                const int sp = wait_next();
+                const double* pp = smem + sp * SD;
+                plane_step(std::integral_constant<int, -1>{}, pp);
+                advance(sp, pp);
+            }
+        }
+        if constexpr (!CARRY) release_s(sm);
+        release_s(sc);
+    }
+#else
     auto wait_full = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
     // This warp is done with sequence number q (position pos of item t). The
     // last of the NW3 warps to release the stage refills it with the plane S
@@ -378,7 +547,6 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
         }
     };
 
-    const int zpm = (int)(wrap_idx(-1, n, a.g.bc) & 1), zpp = (int)(wrap_idx(n, n, a.g.bc) & 1);
     int q0 = 0;  // sequence number of position 0 of the current item
     for (long t = blockIdx.x; t < nitems; t += G) {
         const Item3 it = item3<IY>(t, n, rows);
@@ -438,6 +606,7 @@ __global__ void __launch_bounds__(NT3, EK_LB3) k_tma3d(const KArgs a, const __gr
         release(q0 + it.L + 1, t, it, it.L + 1);
         q0 += it.L + 2;
     }
+#endif
     reduce_and_finalize<EV, EP, NQ, NT3, RP>(a, acc, xsa);
 }
 
