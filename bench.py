@@ -164,11 +164,24 @@ def leja_bytes(prof):
     alg, pas, launches = 0, 0, 0
     freeze = prof.get("freeze", [])
     for m in range(1, prof.get("iters", 0) + 1):
-        k_act = sum(1 for f in freeze if f >= m)
+        # deferred accumulation (ek_leja_run_seq): the iteration moves no
+        # accumulator; ek_leja_combine forms them afterwards (combine_bytes)
+        k_act = 0 if prof.get("deferred") else sum(1 for f in freeze if f >= m)
         alg += per_vec * ((4 if prof["fd"] else 2) + 2 * k_act)
         pas += per_vec * ((3 if prof["fd"] else 2) + 2 * k_act)
         launches += 1
     return alg, pas, launches
+
+
+def combine_bytes(prof):
+    """Bytes of the deferred-accumulation pass of one call: it reads the
+    iterates y_0 .. y_M once (M = the last iteration any accumulator took a
+    term from) and writes the k accumulators."""
+    if not prof.get("deferred") or not prof.get("iters"):
+        return 0
+    freeze = prof.get("freeze", [])
+    last = max(freeze) if freeze else prof["iters"]
+    return 8 * prof["n"] * (last + 1 + prof["k"])
 
 
 def run_ours(args, rank, world, local):
@@ -255,12 +268,19 @@ def run_ours(args, rank, world, local):
 
     # roofline of the fused Leja iteration kernel, live from the timed region
     kb, kp, kl, kt = 0, 0, 0, 0.0
+    cb, cl, ct = 0, 0, 0.0  # the deferred-accumulation passes
+    deferred = any(p.get("deferred") for p in prof)
     for p in prof:
         b, bp, l_ = leja_bytes(p)
         kb += b
         kp += bp
         kl += l_
         kt += sum(s.elapsed_time(e) for s, e in p["events"]) / 1e3
+        cev = p.get("combine_events") or []
+        if cev and p.get("iters"):
+            cb += combine_bytes(p)
+            cl += len(cev)
+            ct += sum(s.elapsed_time(e) for s, e in cev) / 1e3
     peak, peak_kind = peaks()
     achieved = kb / kt / 1e9 if kt > 0 else None
     traffic = None
@@ -272,11 +292,19 @@ def run_ours(args, rank, world, local):
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None, "traffic": traffic,
-            "kernel": "k_march2d<PBruss<true>, EV_FD, EP_LEJA, K, S> (bulk-copy row march "
-                      "with a producer warp): fused FD Jv + Leja recurrence + k accumulators "
-                      "+ ||y||^2 + device freeze test",
-            "bytes_model": "algorithmic, SURVEY.md §8(d) d3: 8*N*(4+2*k_active) per launch "
-                           "(reads u, f(u_n), y, p_1..k; writes y', p_1..k), N = 2*n^2",
+            "kernel": ("k_march2d<PBruss<true>, EV_FD, EP_LEJA, K = 0, S> (bulk-copy row march "
+                       "with a producer warp): fused FD Jv + Leja recurrence + ||y||^2 + device "
+                       "freeze test; the k accumulators are formed once per call by "
+                       "k_leja_combine (deferred accumulation, see `combine`)") if deferred else
+                      ("k_march2d<PBruss<true>, EV_FD, EP_LEJA, K, S> (bulk-copy row march "
+                       "with a producer warp): fused FD Jv + Leja recurrence + k accumulators "
+                       "+ ||y||^2 + device freeze test"),
+            "bytes_model": ("algorithmic, SURVEY.md §8(d) d3 with k = 0: 8*N*4 per launch (reads "
+                            "u, f(u_n), y; writes y'), N = 2*n^2 — the accumulator traffic "
+                            "8*N*2*k_active per iteration of d3 is replaced by one pass per "
+                            "call (`combine`)") if deferred else
+                           ("algorithmic, SURVEY.md §8(d) d3: 8*N*(4+2*k_active) per launch "
+                            "(reads u, f(u_n), y, p_1..k; writes y', p_1..k), N = 2*n^2"),
             "achieved_pass_bytes": kp / kt / 1e9 if kt > 0 else None,
             "frac_pass_bytes": kp / kt / 1e9 / peak if kt > 0 else None,
             "frac_note": "frac uses SURVEY's algorithmic bytes, which count a read of f(u_n) "
@@ -288,6 +316,16 @@ def run_ours(args, rank, world, local):
             "launches": kl, "avg_launch_ms": kt / kl * 1e3 if kl else None,
             "share_of_step": kt / elapsed if elapsed else None,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    if deferred:
+        roof["deferred_accumulation"] = True
+        roof["combine"] = {
+            "kernel": "k_leja_combine: p_i = sum_m d_i[m] y_m per element in registers, "
+                      "the reference's order and roundings",
+            "bytes_model": "8*N*(M+1+k) per call: reads y_0..y_M, writes p_1..k",
+            "launches": cl, "avg_launch_ms": ct / cl * 1e3 if cl else None,
+            "achieved": cb / ct / 1e9 if ct > 0 else None,
+            "frac": cb / ct / 1e9 / peak if ct > 0 else None,
+            "share_of_step": ct / elapsed if elapsed else None}
 
     out = {"metric": METRIC, "value": total_jv / elapsed, "unit": "Jv/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -333,6 +333,36 @@ int ek_leja_call(const ek_grid* g, int jac, const double* u, const double* fu,
                  const double* nu_dev, int fold, int lazy0, int m_end, double gamma,
                  ek_leja_state* st, double* work, void* stream);
 
+/* Deferred accumulation (whole-grid path, large grids). The reference adds
+ * the term d_i[m] y_m to every live accumulator inside the iteration
+ * (leja.py:179), which costs 2k vector transfers per iteration. Here the
+ * iterations m_begin .. m_begin + count - 1 read y_{m-1} from yin[i], write
+ * y_m to yout[i] (one buffer per iterate) and leave the accumulators alone;
+ * the freeze decisions are taken over the state block's k as in
+ * ek_leja_run. ek_leja_combine then forms
+ *     p_i = ((d_i[0] y_0 + d_i[1] y_1) + d_i[2] y_2) + ...
+ * per element in registers, in the reference's order and with its two
+ * roundings per term, up to the iteration at which accumulator i froze
+ * (read from the state block on the device): bit for bit the accumulators of
+ * ek_leja_run, with M + 1 + k vector transfers per call instead of 2kM.
+ * y[j] is the iterate of table column j of the chunk starting at iteration
+ * chunk_base (first chunk: y[0] = b); cont = 1 continues sums that already
+ * hold the earlier chunks. ek_leja_call_seq = ek_leja_call with a folded
+ * begin pass followed by ek_leja_run_seq(count) from m = 1. */
+int ek_leja_run_seq(const ek_grid* g, int jac, const double* u, const double* fu,
+                    const double* const* yin, double* const* yout, int count,
+                    const double* coef_dev, int chunk_base, int m_begin, double gamma,
+                    ek_leja_state* st, double* work, void* stream);
+int ek_leja_combine(int64_t len, const double* const* y, int ny, double* const* p, int k,
+                    const double* coef_dev, int chunk_base, int cont,
+                    const ek_leja_state* st, void* stream);
+int ek_leja_call_seq(const ek_grid* g, int jac, const double* u, const double* fu,
+                     const double* b, const double* const* yin, double* const* yout,
+                     int count, double* const* p, int k, const double* coef_host,
+                     double* coef_dev, double tol, double nu, const double* nu_dev,
+                     int lazy0, double gamma, ek_leja_state* st, double* work,
+                     void* stream);
+
 /* One recurrence step for a Jacobian action computed elsewhere (dense,
  * callable or 1-D operators): y' = jv/gamma - shift*y, accumulators, norm,
  * freeze test (leja.py:172-184). */

@@ -114,6 +114,11 @@ _SIGS = {
                          _I, _I, _D, _P, _P, _PP, _P]),
     "ek_leja_run_graph": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _P, _I,
                                _I, _I, _D, _P, _P, _P]),
+    "ek_leja_run_seq": (_I, [C.POINTER(Grid), _I, _P, _P, _PP, _PP, _I, _P, _I, _I, _D, _P, _P,
+                             _P]),
+    "ek_leja_combine": (_I, [_L, _PP, _I, _PP, _I, _P, _I, _I, _P, _P]),
+    "ek_leja_call_seq": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _PP, _I, _PP, _I, _P, _P,
+                              _D, _D, _P, _I, _D, _P, _P, _P]),
     "ek_leja_update": (_I, [_L, _P, _P, _P, _PP, _I, _P, _I, _I, _D, _I, _P,
                             _P, _P]),
     "ek_power_run": (_I, [C.POINTER(Grid), _I, _P, _P, _P, _PP, _I, _I, _P, _P,

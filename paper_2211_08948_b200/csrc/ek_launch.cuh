@@ -122,7 +122,8 @@ constexpr int tma_stages() {
 template <int EV, int EP, int NC, int K>
 constexpr int tma_stages2() {
     constexpr int bytes = stage2_doubles<EV, EP, NC, K>() * 8;
-    constexpr int two = (110 * 1024) / bytes;
+    // per-block budget: 220 KB of shared memory over the resident blocks
+    constexpr int two = (220 * 1024 / march2_lb<EP, K>()) / bytes;
 #ifdef EK_MARCH_S
     return EK_MARCH_S;
 #else
@@ -418,6 +419,9 @@ template <class P, int EV, int EP>
 inline int launch_p(const KArgs& a, cudaStream_t s) {
     if constexpr (EP == EP_LEJA) {
         switch (a.nk) {
+            // deferred accumulation (ek_leja_run_seq): the iteration only
+            // advances the recurrence, ek_leja_combine forms the sums
+            case 0: return launch_k<P, EV, EP, 0>(a, s);
             case 1: return launch_k<P, EV, EP, 1>(a, s);
             case 2: return launch_k<P, EV, EP, 2>(a, s);
             case 3: return launch_k<P, EV, EP, 3>(a, s);

@@ -31,15 +31,26 @@ constexpr int W2 = 256;    // columns per strip
 constexpr int T2 = 256;    // compute threads: one column each
 constexpr int NW2 = T2 / 32;
 #ifndef EK_TIGHT2
-#define EK_TIGHT2 1  // 1: the row loop without per-row divisions (producer-warp build)
+#define EK_TIGHT2 1  // 1: K = 0 Leja instance: row loop without per-row divisions
 #endif
 #ifndef EK_WAIT2_NS
-#define EK_WAIT2_NS 1000  // > 0: suspend-time hint (ns) of the row waits' try_wait
+#define EK_WAIT2_NS 0  // > 0: suspend-time hint (ns) of the row waits' try_wait (measured: none is best)
 #endif
 #ifndef EK_PROD2
 #define EK_PROD2 1  // 1: one extra producer warp issues the row copies
 #endif
 constexpr int NT2 = T2 + (EK_PROD2 ? 32 : 0);  // threads per block
+// Resident blocks per SM the register budget is sized for. The Leja
+// iteration without accumulators (K = 0, deferred accumulation) moves so few
+// bytes per point that it is bound by its fp64 dependency chains, not by
+// DRAM: a third block per SM gives the schedulers the warps to hide them.
+#ifndef EK_MARCH_LB0
+#define EK_MARCH_LB0 3
+#endif
+template <int EP, int K>
+__host__ __device__ constexpr int march2_lb() {
+    return (EP == EP_LEJA && K == 0) ? EK_MARCH_LB0 : 2;
+}
 constexpr int RAW2 = 272;  // doubles per raw row slot: element e <-> column j0 - 2 + e
 constexpr int CTR2 = 256;  // doubles per centre row slot
 
@@ -209,7 +220,7 @@ __host__ __device__ __forceinline__ int march2_segs(long G, int ns) {
 }
 
 template <class P, int EV, int EP, int K, int S, int RP>
-__global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
+__global__ void __launch_bounds__(NT2, (march2_lb<EP, K>())) k_march2d(const KArgs a) {
     static_assert(S >= 4, "row ring needs i-1, i, i+1 and one in flight");
     constexpr int NC = P::NC, NQ = nq_of<EV, EP>();
     constexpr int NR = nraw<EV>();
@@ -293,83 +304,87 @@ __global__ void __launch_bounds__(NT2, 2) k_march2d(const KArgs a) {
     }
 #endif
 
-#if EK_PROD2 && EK_TIGHT2
-    // Tight row loop (producer-warp build): the ring position is a stage
-    // index plus one phase bit per stage — every sequence number is waited
-    // for exactly once by each warp, in order — so the loop carries no
-    // division; a warp whose row has not landed sleeps in the barrier unit
-    // (try_wait with a suspend-time hint) instead of spinning.
-    int sn = 0;         // stage of the next sequence number this warp waits for
-    uint32_t ph = 0;    // bit s: parity of that wait on stage s
-    auto wait_next = [&]() {
-        const int s = sn;
-        mbar_wait_ns<EK_WAIT2_NS>(&full[s], (ph >> s) & 1u);
-        ph ^= 1u << s;
-        sn = s + 1 == S ? 0 : s + 1;
-        return s;
-    };
-    auto release_s = [&](int s) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-    };
-    for (long tt = blockIdx.x; tt < nitems; tt += G) {
-        const Item2 it = item2(tt, ns, ng, rows);
-        const int j = it.j0 + t;
-        const bool live = j < cols;
-        int sm = wait_next(), sc = wait_next();
-        const double* pm = smem + sm * SD;
-        const double* pc = smem + sc * SD;
-        long i = it.r0;
-        for (int p = 1; p <= it.L; ++p, ++i) {
-            const int sp = wait_next();
-            const double* pp = smem + sp * SD;
-            if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs);
-            release_s(sm);
-            sm = sc; sc = sp; pm = pc; pc = pp;
-        }
-        release_s(sm);
-        release_s(sc);
-    }
-#else
-    auto wait_full = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
-    auto release = [&](int q, const Item2& it, int pos) {
-        __syncwarp();
-        if (lane == 0) {
-            const int s = q % S;
+    // (the K = 0 Leja instance only: measured neutral for the DRAM-bound ones)
 #if EK_PROD2
-            (void)it; (void)pos;
-            mbar_arrive(&empty[s]);
-#else
-            if ((atomicAdd(&released[s], 1) + 1) % NW2 == 0) issue_ahead(it, pos, s);
-#endif
-        }
-    };
-
-    int q0 = 0;  // sequence number of position 0 of the current item
-    for (long tt = blockIdx.x; tt < nitems; tt += G) {
-        const Item2 it = item2(tt, ns, ng, rows);
-        const int j = it.j0 + t;
-        const bool live = j < cols;
-        wait_full(q0);
-        wait_full(q0 + 1);
-        int sm = q0 % S, sc = (q0 + 1) % S;
-        for (int p = 1; p <= it.L; ++p) {
-            wait_full(q0 + p + 1);
-            const int sp = sc + 1 == S ? 0 : sc + 1;
+    if constexpr (EK_TIGHT2 && EP == EP_LEJA && K == 0) {
+        // Tight row loop (producer-warp build): the ring position is a stage
+        // index plus one phase bit per stage — every sequence number is waited
+        // for exactly once by each warp, in order — so the loop carries no
+        // division; a warp whose row has not landed sleeps in the barrier unit
+        // (try_wait with a suspend-time hint) instead of spinning.
+        int sn = 0;         // stage of the next sequence number this warp waits for
+        uint32_t ph = 0;    // bit s: parity of that wait on stage s
+        auto wait_next = [&]() {
+            const int s = sn;
+            mbar_wait_ns<EK_WAIT2_NS>(&full[s], (ph >> s) & 1u);
+            ph ^= 1u << s;
+            sn = s + 1 == S ? 0 : s + 1;
+            return s;
+        };
+        auto release_s = [&](int s) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        };
+        for (long tt = blockIdx.x; tt < nitems; tt += G) {
+            const Item2 it = item2(tt, ns, ng, rows);
+            const int j = it.j0 + t;
+            const bool live = j < cols;
+            int sm = wait_next(), sc = wait_next();
             const double* pm = smem + sm * SD;
             const double* pc = smem + sc * SD;
-            const double* pp = smem + sp * SD;
-            const long i = it.r0 + p - 1;
-            if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs);
-            release(q0 + p - 1, it, p - 1);
-            sm = sc;
-            sc = sp;
+            long i = it.r0;
+            for (int p = 1; p <= it.L; ++p, ++i) {
+                const int sp = wait_next();
+                const double* pp = smem + sp * SD;
+                if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs);
+                release_s(sm);
+                sm = sc; sc = sp; pm = pc; pc = pp;
+            }
+            release_s(sm);
+            release_s(sc);
         }
-        release(q0 + it.L, it, it.L);
-        release(q0 + it.L + 1, it, it.L + 1);
-        q0 += it.L + 2;
-    }
+    } else
 #endif
+    {
+        auto wait_full = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
+        auto release = [&](int q, const Item2& it, int pos) {
+            __syncwarp();
+            if (lane == 0) {
+                const int s = q % S;
+#if EK_PROD2
+                (void)it; (void)pos;
+                mbar_arrive(&empty[s]);
+#else
+                if ((atomicAdd(&released[s], 1) + 1) % NW2 == 0) issue_ahead(it, pos, s);
+#endif
+            }
+        };
+
+        int q0 = 0;  // sequence number of position 0 of the current item
+        for (long tt = blockIdx.x; tt < nitems; tt += G) {
+            const Item2 it = item2(tt, ns, ng, rows);
+            const int j = it.j0 + t;
+            const bool live = j < cols;
+            wait_full(q0);
+            wait_full(q0 + 1);
+            int sm = q0 % S, sc = (q0 + 1) % S;
+            for (int p = 1; p <= it.L; ++p) {
+                wait_full(q0 + p + 1);
+                const int sp = sc + 1 == S ? 0 : sc + 1;
+                const double* pm = smem + sm * SD;
+                const double* pc = smem + sc * SD;
+                const double* pp = smem + sp * SD;
+                const long i = it.r0 + p - 1;
+                if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs);
+                release(q0 + p - 1, it, p - 1);
+                sm = sc;
+                sc = sp;
+            }
+            release(q0 + it.L, it, it.L);
+            release(q0 + it.L + 1, it, it.L + 1);
+            q0 += it.L + 2;
+        }
+    }
     reduce_and_finalize<EV, EP, NQ, NT2, RP>(a, acc, xsa);
 }
 

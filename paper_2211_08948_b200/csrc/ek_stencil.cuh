@@ -958,7 +958,7 @@ __device__ void finalize(const KArgs& a, const double* tot, const XAcc* xt) {
         }
         const int m = a.m < 0 ? st->m + 1 : a.m;
         const int mi = a.m < 0 ? m - a.chunk_base : a.mi;
-        leja_decide(st, a.coef, mi, m, a.nk, tot[0], tot[1], EV == EV_FD);
+        leja_decide(st, a.coef, mi, m, a.nk > 0 ? a.nk : st->k, tot[0], tot[1], EV == EV_FD);
         if (a.cond_on)  // another turn of the graph loop?
             cudaGraphSetConditional(a.cond, (!st->done && m + 1 < a.m_limit &&
                                              m + 1 - a.chunk_base < 32) ? 1u : 0u);

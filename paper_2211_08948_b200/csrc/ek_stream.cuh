@@ -95,7 +95,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // The same wait with a suspend-time hint of NS nanoseconds: a warp whose
 // stage has not landed sleeps in the barrier unit instead of spinning
 // through issue slots the other warps need (NS = 0: plain try_wait loop).
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
 template <int NS>
 __device__ __forceinline__ void mbar_wait_ns(uint64_t* bar, uint32_t parity) {
     if constexpr (NS > 0) {
@@ -106,8 +105,6 @@ __device__ __forceinline__ void mbar_wait_ns(uint64_t* bar, uint32_t parity) {
             "@!P1 bra LAB_WAITH;\n}" ::"r"(smem_u32(bar)),
             "r"(parity), "r"(NS)
             : "memory");
-    } else if constexpr (NS < 0) {  // A/B: back off with nanosleep between polls
-        while (!mbar_test(bar, parity)) __nanosleep(-NS);
     } else {
         mbar_wait(bar, parity);
     }

@@ -254,6 +254,104 @@ __global__ void __launch_bounds__(TPB) k_leja_fold_done(const LejaVArgs a) {
     }
 }
 
+// Deferred accumulation (ek_leja_run_seq + ek_leja_combine): the iterations
+// of a chunk keep every iterate y_m in its own buffer and leave the
+// accumulators alone; this pass then forms, per element and in registers,
+//     p_i = ((d_i[0] y_0 + d_i[1] y_1) + d_i[2] y_2) + ...   (leja.py:161, 179)
+// term by term in the reference's order with the same two roundings per term
+// (product, sum; the library is built without FMA contraction), up to the
+// iteration at which accumulator i froze (state block: freeze[i], or m while
+// it is still active). A call of M iterations and k accumulators then moves
+// M + 1 + k vectors once instead of 2 k per iteration.
+struct LejaCombineArgs {
+    int64_t len;
+    const double* y[33];  // y[j]: the iterate of table column j (first chunk: y[0] = b)
+    int ny;
+    double* p[8];
+    int nk;
+    const double* coef;   // this chunk's table: row 1 + i = d_i, 32 columns
+    int chunk_base;       // iteration of column 0
+    int cont;             // 1: p already holds the sum over the earlier chunks
+    const ek_leja_state* st;
+};
+
+template <int NK>
+__global__ void __launch_bounds__(TPB) k_leja_combine(const LejaCombineArgs a) {
+    __shared__ double d[NK][32];
+    __shared__ int last[NK];  // last column of accumulator i in this chunk (-1: none)
+    // m = 0 result of a folded begin is written by k_leja_fold_done (or stays lazy)
+    if (!a.cont && a.st->done && a.st->iters == 0 && a.st->status == EK_ST_OK) return;
+    for (int t = threadIdx.x; t < NK * 32; t += TPB) {
+        const int q = t >> 5, j = t & 31;
+        d[q][j] = q < a.nk ? a.coef[(1 + q) * 32 + j] : 0.0;
+    }
+    if (threadIdx.x < NK) {
+        const int q = threadIdx.x;
+        int l = -1;
+        if (q < a.nk) {
+            const int ml = ((a.st->active >> q) & 1u) ? a.st->m : a.st->freeze[q];
+            l = ml - a.chunk_base;
+            if (l > a.ny - 1) l = a.ny - 1;
+            if (l < 0) l = -1;
+        }
+        last[q] = l;
+    }
+    __syncthreads();
+    int lq[NK], maxl = -1;
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {
+        lq[q] = last[q];
+        maxl = lq[q] > maxl ? lq[q] : maxl;
+    }
+    if (maxl < 0) return;
+    bool vec = true;
+    for (int j = 0; j <= maxl; ++j) vec = vec && al16d(a.y[j]);
+#pragma unroll
+    for (int q = 0; q < NK; ++q)
+        if (q < a.nk) vec = vec && al16d(a.p[q]);
+    const bool cont = a.cont != 0;
+    EK_FOR4(e0, a.len) {
+        const bool full = vec && e0 + 4 <= a.len;
+        double acc[NK][4];
+#pragma unroll
+        for (int q = 0; q < NK; ++q) {
+            if (cont && lq[q] >= 0) ld4(a.p[q], e0, a.len, full, acc[q]);
+            else {
+#pragma unroll
+                for (int w = 0; w < 4; ++w) acc[q][w] = 0.0;
+            }
+        }
+        // four iterates per turn: their loads are all issued before the
+        // first one is used (128 B in flight per thread)
+        for (int j0 = 0; j0 <= maxl; j0 += 4) {
+            double yv[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (j0 + u <= maxl) ld4(a.y[j0 + u], e0, a.len, full, yv[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + u;
+                if (j <= maxl) {
+                    const bool first = j == 0 && !cont;
+#pragma unroll
+                    for (int q = 0; q < NK; ++q)
+                        if (j <= lq[q]) {
+                            const double dq = d[q][j];
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                const double t = dq * yv[u][w];
+                                acc[q][w] = first ? t : acc[q][w] + t;
+                            }
+                        }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NK; ++q)
+            if (lq[q] >= 0) st4(a.p[q], e0, a.len, full, acc[q]);
+    }
+}
+
 // out = (a*x) + (b*y)
 __global__ void __launch_bounds__(TPB) k_axpby(int64_t n, double a, const double* __restrict__ x,
                                                double b, const double* __restrict__ y,

@@ -655,6 +655,85 @@ int ek_leja_call(const ek_grid* g, int jac, const double* u, const double* fu, c
                        nullptr, stream);
 }
 
+// Deferred accumulation: iterations m_begin .. m_begin + count - 1 with
+// explicit iterate buffers (y_{m-1} in yin[i], y_m into yout[i]) and no
+// accumulator traffic (kernel instances with K = 0); the freeze decisions
+// run over the state block's k as usual.
+int ek_leja_run_seq(const ek_grid* g, int jac, const double* u, const double* fu,
+                    const double* const* yin, double* const* yout, int count,
+                    const double* coef_dev, int chunk_base, int m_begin, double gamma,
+                    ek_leja_state* st, double* work, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (count < 0 || !yin || !yout || !st) {
+        set_error("ek_leja_run_seq: bad arguments (count=%d)", count);
+        return EK_ERR_INVALID;
+    }
+    const int ev = jv_ev(g, jac);
+    if (ev < 0) return EK_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    KArgs a;
+    base_args(a, g, nullptr);
+    a.u = u; a.fu = fu; a.nk = 0; a.coef = coef_dev; a.gamma = mkdv(gamma); a.st = st; a.work = work;
+    for (int i = 0; i < count; ++i) {
+        a.m = m_begin + i;
+        a.mi = a.m - chunk_base;
+        a.y = yin[i];
+        a.out = yout[i];
+        const int rc = launch_stencil<EP_LEJA>(ev, a, s);
+        if (rc != EK_OK) return rc;
+    }
+    return EK_OK;
+}
+
+int ek_leja_combine(int64_t len, const double* const* y, int ny, double* const* p, int k,
+                    const double* coef_dev, int chunk_base, int cont, const ek_leja_state* st,
+                    void* stream) {
+    if (len < 1 || k < 1 || k > 8 || ny < 1 || ny > 33 || !y || !p || !coef_dev || !st) {
+        set_error("ek_leja_combine: bad arguments (k=%d ny=%d)", k, ny);
+        return EK_ERR_INVALID;
+    }
+    LejaCombineArgs a{};
+    a.len = len; a.ny = ny; a.nk = k; a.coef = coef_dev; a.chunk_base = chunk_base;
+    a.cont = cont; a.st = st;
+    for (int j = 0; j < ny; ++j) a.y[j] = y[j];
+    for (int q = 0; q < k; ++q) a.p[q] = p[q];
+    const dim3 grid = vgrid4(len);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (k) {
+        case 1: k_leja_combine<1><<<grid, TPB, 0, s>>>(a); break;
+        case 2: k_leja_combine<2><<<grid, TPB, 0, s>>>(a); break;
+        case 3: k_leja_combine<3><<<grid, TPB, 0, s>>>(a); break;
+        case 4: k_leja_combine<4><<<grid, TPB, 0, s>>>(a); break;
+        default: k_leja_combine<8><<<grid, TPB, 0, s>>>(a); break;
+    }
+    EK_LAUNCH_CHECK("k_leja_combine");
+    return EK_OK;
+}
+
+// ek_leja_call with deferred accumulation: table upload, state init, folded
+// begin pass and the first `count` iterations (ek_leja_run_seq).
+int ek_leja_call_seq(const ek_grid* g, int jac, const double* u, const double* fu,
+                     const double* b, const double* const* yin, double* const* yout, int count,
+                     double* const* p, int k, const double* coef_host, double* coef_dev,
+                     double tol, double nu, const double* nu_dev, int lazy0, double gamma,
+                     ek_leja_state* st, double* work, void* stream) {
+    if (!grid_ok(g)) return EK_ERR_INVALID;
+    if (k < 1 || k > 8 || !coef_host || !coef_dev || !st) {
+        set_error("ek_leja_call_seq: bad arguments (k=%d)", k);
+        return EK_ERR_INVALID;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(coef_dev, coef_host, (size_t)(k + 1) * 32 * sizeof(double),
+                                    cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "ek_leja_call_seq");
+    k_leja_init<<<1, 32, 0, s>>>(st, tol, nu, nu_dev, k, -1, lazy0);
+    EK_LAUNCH_CHECK("k_leja_init");
+    const int rc = ek_leja_begin_len(ek_grid_len(g), b, p, k, coef_dev, st, work, stream);
+    if (rc != EK_OK || count < 1) return rc;
+    return ek_leja_run_seq(g, jac, u, fu, yin, yout, count, coef_dev, 0, 1, gamma, st, work,
+                           stream);
+}
+
 int ek_leja_update(int64_t len, const double* jv, const double* y, double* ynext,
                    double* const* p, int k, const double* coef_dev, int chunk_base, int m,
                    double gamma, int check_jv, ek_leja_state* st, double* work, void* stream) {

@@ -49,6 +49,15 @@ _FASTCALL = os.environ.get("EK_LEJA_FASTCALL", "1") != "0"  # A/B switch (tools)
 # runs to its end or to the 32-point chunk boundary with no launch batch to
 # size. "0" keeps the launch batches (A/B runs, tools).
 _GRAPH = [os.environ.get("EK_LEJA_GRAPH", "1") != "0"]
+# Deferred accumulation (ek_leja_run_seq / ek_leja_combine): on large grids the
+# iterations keep every iterate in its own buffer and one pass forms the
+# accumulators at the end — M + 1 + k vector transfers per call instead of
+# 2kM, the same bits. [on, smallest vector length, smallest group, byte budget
+# of the iterate buffers of one call]
+_DEFER = [os.environ.get("EK_LEJA_DEFER", "1") != "0",
+          int(os.environ.get("EK_LEJA_DEFER_MIN_N", str(1 << 22))),
+          int(os.environ.get("EK_LEJA_DEFER_MIN_K", "2")),
+          int(os.environ.get("EK_LEJA_DEFER_BYTES", str(48 << 30)))]
 
 
 def generate_leja_points(m=DEFAULT_NUM_POINTS, n_candidates=DEFAULT_CANDIDATES):
@@ -427,8 +436,12 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     # fused single-GPU path: the begin pass only takes ||b|| and the m = 0
     # decisions; the first iteration writes p_i = d_i[0] b + d_i[1] y_1
     fold = Jn is not None and not slab and max_points > 1
+    # deferred accumulation: large whole-grid calls (bandwidth-bound); the
+    # iterate buffers of one chunk must fit the byte budget
+    da = bool(fold and _DEFER[0] and n >= _DEFER[1] and k >= _DEFER[2]
+              and min(_CHUNK, max_points) * n * 8 <= _DEFER[3])
     # graph mode: one graph launch covers the whole first chunk
-    graph = fold and _FASTCALL and _GRAPH[0]
+    graph = fold and _FASTCALL and _GRAPH[0] and not da
     # (speculate only when the group's previous count fits the first chunk: a
     # call that crosses a chunk needs the host for its next table)
     spec = _spec is not None and fold and min(_CHUNK, max_points) > int(_first_batch)
@@ -445,7 +458,36 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     ws = D.work_ptr(N.lib().ek_workspace_bytes(C.byref(Jn.grid)) if Jn else None)
     pp = N.ptrs(ps)
     ybuf = None
-    if fast:
+    # deferred accumulation: Y[j] = the iterate of table column j of the
+    # current chunk (first chunk: Y[0] = b), yprev = the last iterate of the
+    # previous chunk, pool = buffers free for reuse
+    Y, yprev, pool = [bd] + [None] * (_CHUNK - 1), None, []
+
+    def seq_buffers(m0, m1, base_):
+        """Input / output buffers of iterations m0 .. m1-1 (chunk base base_)."""
+        yin, yout = [], []
+        for mm in range(m0, m1):
+            j = mm - base_
+            yin.append(Y[j - 1] if j >= 1 else yprev)
+            Y[j] = pool.pop() if pool else D.empty(n)
+            yout.append(Y[j])
+        return N.ptrs(yin), N.ptrs(yout)
+
+    def combine(base_):
+        ny = max(j for j in range(_CHUNK) if Y[j] is not None) + 1
+        N.check(N.lib().ek_leja_combine(
+            n, N.ptrs(Y[:ny]), ny, pp, k, C.c_void_p(table.dev.data_ptr()), base_,
+            1 if base_ > 0 else 0, st.ptr, D.stream()), "ek_leja_combine")
+
+    if fast and da and not spec_zero:
+        yin0, yout0 = seq_buffers(1, first_hi, 0)
+        N.check(N.lib().ek_leja_call_seq(
+            C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()), C.c_void_p(Jn.fu.data_ptr()),
+            C.c_void_p(bd.data_ptr()), yin0, yout0, first_hi - 1, pp, k,
+            table.host.ctypes.data_as(C.c_void_p), C.c_void_p(table.dev.data_ptr()), float(tol),
+            nu, nu_ptr, 1 if lazy else 0, float(gamma), st.ptr, ws, D.stream()),
+            "ek_leja_call_seq")
+    elif fast:
         ybuf = None if spec_zero else [D.empty(n), D.empty(n)]
         N.check(N.lib().ek_leja_call(
             C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()), C.c_void_p(Jn.fu.data_ptr()),
@@ -480,15 +522,16 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
         return LejaResult(vectors=[float(dds[i][0]) * D.V(bd) for i in range(k)],
                           iters=None, freeze_iters=None)
 
-    if ybuf is None:
+    if ybuf is None and not da:
         ybuf = [D.empty(n), D.empty(n)]
-    yp = N.ptrs(ybuf)
+    yp = N.ptrs(ybuf or [])
     fd_seen = 0
     m = 1
     base = 0
     prof = None
     if PROFILE is not None and Jn is not None:
-        prof = {"events": [], "k": k, "n": n, "fd": Jn.jac == N.JAC_FD}
+        prof = {"events": [], "k": k, "n": n, "fd": Jn.jac == N.JAC_FD, "deferred": da,
+                "launches": [], "combine_events": []}
         PROFILE.append(prof)
     while m < max_points:
         if m >= m_avail:  # next 32-point chunk (leja.py:168-171)
@@ -496,6 +539,12 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             for ci in coeffs:  # keep the pool one chunk ahead
                 _dd_prefetch(l, ci * h, est, xi, min(m_avail + _CHUNK, max_points))
             dds = [_dd_cached(l, ci * h, est, xi, m_avail) for ci in coeffs]
+            if da:  # fold the finished chunk into the sums before its table goes
+                combine(base)
+                yprev = Y[m - 1 - base]
+                pool.extend(y for j, y in enumerate(Y)
+                            if y is not None and y is not yprev and y is not bd)
+                Y = [None] * _CHUNK
             base = m
             table.load(base, m_avail, dds, c, gamma, xi)
         if Jn is not None:
@@ -505,8 +554,17 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             if prof is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
+            if prof is not None:
+                prof["launches"].append(hi - m)
             if fast and m == 1:
-                pass  # launched by ek_leja_call
+                pass  # launched by ek_leja_call / ek_leja_call_seq
+            elif da:
+                yin_, yout_ = seq_buffers(m, hi, base)
+                N.check(N.lib().ek_leja_run_seq(
+                    C.byref(Jn.grid), Jn.jac, C.c_void_p(Jn.u.data_ptr()),
+                    C.c_void_p(Jn.fu.data_ptr()), yin_, yout_, hi - m,
+                    C.c_void_p(table.dev.data_ptr()), base, m, float(gamma), st.ptr, ws,
+                    D.stream()), "ek_leja_run_seq")
             elif slab and Jn.comm.peer:
                 # peer mode: ghost rows of b once (NCCL), then every pass
                 # stores its boundary rows into the neighbours' windows and
@@ -545,6 +603,16 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             if prof is not None:
                 ev[1].record()
                 prof["events"].append(ev)
+            if spec and da:
+                # the freeze points are read from the state block on the device
+                if prof is not None:
+                    cev = (torch.cuda.Event(enable_timing=True),
+                           torch.cuda.Event(enable_timing=True))
+                    cev[0].record()
+                combine(base)
+                if prof is not None:
+                    cev[1].record()
+                    prof["combine_events"].append(cev)
             if spec:
                 def on_state(hst, prof=prof):
                     if hst.status != N.ST_OK or not hst.done:
@@ -591,6 +659,15 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                 # everything froze at m = 0: ps[i] = dds[i][0] * y (leja.py:161)
                 return LejaResult(vectors=[float(dds[i][0]) * D.V(bd) for i in range(k)],
                                   iters=0, freeze_iters=[0] * k)
+            if da:
+                if prof is not None:
+                    cev = (torch.cuda.Event(enable_timing=True),
+                           torch.cuda.Event(enable_timing=True))
+                    cev[0].record()
+                combine(base)
+                if prof is not None:
+                    cev[1].record()
+                    prof["combine_events"].append(cev)
             return LejaResult(vectors=[D.like_input(p, b) for p in ps],
                               iters=int(hst.iters),
                               freeze_iters=[int(hst.freeze[i]) for i in range(k)])

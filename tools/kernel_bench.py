@@ -28,6 +28,9 @@ def main():
                     help="2 row march (default), 1 32x8 chunks, 0 register-staged")
     ap.add_argument("--kiops", action="store_true")
     ap.add_argument("--reps", type=int, default=5, help="timed repetitions (median)")
+    ap.add_argument("--defer", type=int, default=None,
+                    help="1 / 0: force deferred accumulation on / off (default: the "
+                         "library's own choice by size and group)")
     ap.add_argument("--repro", action="store_true",
                     help="order-independent sums (ek_set_repro): the RP = 1 kernel instances")
     args = ap.parse_args()
@@ -42,6 +45,9 @@ def main():
     if args.tma_mode is not None:
         NAT.lib().ek_set_tma(args.tma_mode)
 
+    if args.defer is not None:
+        L._DEFER[0] = bool(args.defer)
+        L._DEFER[1], L._DEFER[2] = 0, 1
     prob = ext.make_ext_problem(args.problem, n=args.n)
     rhs = ek.CountingRhs(prob.rhs)
     sys_ = ek.make_linearized(rhs, prob.u0, jac_factory=prob.jac_factory)
@@ -77,10 +83,13 @@ def main():
     # state-dependent analytic (Burgers) u, y; + k accumulators read and
     # written, y' written. The FD pass itself re-evaluates f(u_n) (one vector less).
     base = 4 if fd else (2 if lin else 3)
-    per = 8 * n * (base + 2 * args.k)
+    deferred = bool(prof[0].get("deferred"))
+    # deferred accumulation: the iteration moves no accumulator (the call ends
+    # by max_points here, so the combine pass is not part of this timing)
+    per = 8 * n * (base + (0 if deferred else 2 * args.k))
     per_pass = per - (8 * n if fd else 0)
     out = {"problem": args.problem, "tma_mode": args.tma_mode, "repro": bool(args.repro),
-           "n": args.n, "dofs": n, "k": args.k, "iters": args.iters,
+           "n": args.n, "dofs": n, "k": args.k, "iters": args.iters, "deferred": deferred,
            "ms_per_launch": t / args.iters * 1e3, "bytes_per_launch": per,
            "GBps": per * args.iters / t / 1e9, "GBps_pass": per_pass * args.iters / t / 1e9,
            "ms_per_launch_reps": [round(x / args.iters * 1e3, 4) for x in ts]}
