@@ -168,7 +168,9 @@ def leja_bytes(prof):
         # accumulator; ek_leja_combine forms them afterwards (combine_bytes)
         k_act = 0 if prof.get("deferred") else sum(1 for f in freeze if f >= m)
         alg += per_vec * ((4 if prof["fd"] else 2) + 2 * k_act)
-        pas += per_vec * ((3 if prof["fd"] else 2) + 2 * k_act)
+        # (the K = 0 FD iteration streams the stored f(u_n): it moves all 4)
+        pas += per_vec * ((4 if prof.get("deferred") else 3) if prof["fd"] else 2) \
+            + per_vec * 2 * k_act
         launches += 1
     return alg, pas, launches
 
@@ -307,12 +309,16 @@ def run_ours(args, rank, world, local):
                             "(reads u, f(u_n), y, p_1..k; writes y', p_1..k), N = 2*n^2"),
             "achieved_pass_bytes": kp / kt / 1e9 if kt > 0 else None,
             "frac_pass_bytes": kp / kt / 1e9 / peak if kt > 0 else None,
-            "frac_note": "frac uses SURVEY's algorithmic bytes, which count a read of f(u_n) "
-                         "that the fused pass replaces by re-evaluating f from the u "
-                         "neighbourhood it reads anyway, so frac can exceed 1; "
-                         "frac_pass_bytes is the fraction on the bytes the pass moves",
-            "pass_bytes_model": "8*N*(3+2*k_active): the bytes this kernel moves (f(u_n) is "
-                                "re-evaluated from the u neighbourhood instead of read)",
+            "frac_note": ("deferred accumulation: the K = 0 iteration streams the stored f(u_n), "
+                          "so the bytes it moves are SURVEY's algorithmic bytes with k = 0 and "
+                          "frac_pass_bytes = frac") if deferred else
+                         ("frac uses SURVEY's algorithmic bytes, which count a read of f(u_n) "
+                          "that the fused pass replaces by re-evaluating f from the u "
+                          "neighbourhood it reads anyway, so frac can exceed 1; "
+                          "frac_pass_bytes is the fraction on the bytes the pass moves"),
+            "pass_bytes_model": ("8*N*4: u, f(u_n), y read, y' written") if deferred else
+                                ("8*N*(3+2*k_active): the bytes this kernel moves (f(u_n) is "
+                                 "re-evaluated from the u neighbourhood instead of read)"),
             "launches": kl, "avg_launch_ms": kt / kl * 1e3 if kl else None,
             "share_of_step": kt / elapsed if elapsed else None,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}

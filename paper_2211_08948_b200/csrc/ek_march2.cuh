@@ -54,9 +54,30 @@ __host__ __device__ constexpr int march2_lb() {
 constexpr int RAW2 = 272;  // doubles per raw row slot: element e <-> column j0 - 2 + e
 constexpr int CTR2 = 256;  // doubles per centre row slot
 
+// The FD passes re-evaluate f(u_n) from the u neighbourhood they stage anyway
+// instead of streaming it (one vector less to move). The Leja iteration
+// without accumulators (K = 0) is bound by its fp64 work, not by DRAM, so
+// that instance streams the stored f(u_n) as a centre field instead and
+// evaluates f once per point.
+#ifndef EK_FD_READFU
+#define EK_FD_READFU 1
+#endif
+template <int EV, int EP, int K>
+__host__ __device__ constexpr bool march_rfu() {
+    return EK_FD_READFU && EV == EV_FD && EP == EP_LEJA && K == 0;
+}
+template <int EV, int EP, int K>
+__host__ __device__ constexpr bool march_fu() {
+    return needs_fu<EV>() || march_rfu<EV, EP, K>();
+}
+template <int EV, int EP, int K>
+__host__ __device__ constexpr int nctr2() {
+    return nctr_maps<EV, EP, K>() + (march_rfu<EV, EP, K>() ? 1 : 0);
+}
+
 template <int EV, int EP, int NC, int K>
 __host__ __device__ constexpr int stage2_doubles() {
-    return nraw<EV>() * NC * RAW2 + nctr_maps<EV, EP, K>() * NC * CTR2;
+    return nraw<EV>() * NC * RAW2 + nctr2<EV, EP, K>() * NC * CTR2;
 }
 
 // Work items: strip s (columns s*W2 ..) x row segment g (rows
@@ -111,8 +132,8 @@ __device__ __forceinline__ const double* ctr_field(const KArgs& a, int g) {
 template <int EV, int EP, int NC, int K>
 __device__ __forceinline__ void issue_row(const KArgs& a, double* buf, uint64_t* bar,
                                           const Item2& it, int pos, int rows, uint32_t active) {
-    constexpr int NR = nraw<EV>(), NCM = nctr_maps<EV, EP, K>();
-    constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    constexpr int NR = nraw<EV>(), NCM = nctr2<EV, EP, K>();
+    constexpr int FU = march_fu<EV, EP, K>() ? 1 : 0;
     const int i = it.r0 - 1 + pos;
     const bool centre = pos >= 1 && pos <= it.L;
     const long cols = a.g.n;
@@ -152,7 +173,8 @@ __device__ __forceinline__ void issue_row(const KArgs& a, double* buf, uint64_t*
 #pragma unroll
         for (int g = 0; g < NCM; ++g)
             if (g < FU || ((active >> (g - FU)) & 1u)) {
-                const double* fb = ctr_field<EV, EP>(a, g);
+                const double* fb = (march_rfu<EV, EP, K>() && g == 0) ? a.fu
+                                                                      : ctr_field<EV, EP>(a, g);
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
                     bulk_g2s_hint(ctr + (g * NC + c) * CTR2, fb + c * a.npts + (long)i * cols + it.j0,
@@ -168,7 +190,7 @@ __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, con
                                              const double* pc, const double* pp, long i, int j,
                                              int t, int cols, double* acc, XS xs) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
-    constexpr int FU = needs_fu<EV>() ? 1 : 0;
+    constexpr int FU = march_fu<EV, EP, K>() ? 1 : 0;
     Nb nb[NC][NCH];
     double yc[NC];
 #pragma unroll
@@ -209,7 +231,7 @@ __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, con
         if constexpr (EP == EP_REM && K > 0) z.p[0][c] = ctr[(FU * NC + c) * CTR2 + t];
     }
     double val[NC];
-    evaluate<P, EV, NCH>(a, ctl, nb, z.fu, val, z.jbad);
+    evaluate<P, EV, NCH, march_rfu<EV, EP, K>()>(a, ctl, nb, z.fu, val, z.jbad);
     epilogue<EV, EP, NC, K>(a, ctl, i * cols + j, val, z, acc, xs);
 }
 

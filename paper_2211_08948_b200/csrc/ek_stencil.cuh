@@ -373,7 +373,9 @@ __device__ __forceinline__ void fetch(const Ctl& ctl, const double* pu, const do
 }
 
 // Value at the centre from the channel neighbourhoods; fuc = f(u_n) there.
-template <class P, int EV, int NCH>
+// RFU (EV_FD only): take f(u_n) from fuc — the stored RHS vector, the same
+// bits — instead of evaluating it again from the u neighbourhood.
+template <class P, int EV, int NCH, bool RFU = false>
 __device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
                                          const Nb (&nb)[P::NC][NCH],
                                          const double (&fuc)[P::NC], double (&val)[P::NC],
@@ -390,7 +392,12 @@ __device__ __forceinline__ void evaluate(const KArgs& a, const Ctl& ctl,
         for (int c = 0; c < NC; ++c) { s[c] = nb[c][0]; su[c] = nb[c][1]; }
         double fw[NC], fu[NC];
         P::f(s, fw, a.pc);
-        P::f(su, fu, a.pc);  // f(u_n), bit-identical to the RHS pass
+        if constexpr (RFU) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) fu[c] = fuc[c];
+        } else {
+            P::f(su, fu, a.pc);  // f(u_n), bit-identical to the RHS pass
+        }
 #pragma unroll
         for (int c = 0; c < NC; ++c)
             val[c] = ctl.y_zero ? 0.0 : dv(fw[c] - fu[c], ctl.eps_d);  // linalg.py:126
