@@ -254,11 +254,11 @@ def run_ours(args, rank, world, local):
         e1.record()
         torch.cuda.synchronize()
     launches = N.lib().ek_launch_count() - launches0
-    if L._GRAPH[0]:
-        # graph mode: the library counts one launch per Leja graph; the kernels
-        # its device-side loop ran are the call's iterations
-        launches += counts["leja"]
     prof, L.PROFILE = L.PROFILE, None
+    # graph mode: the library counts one launch per Leja graph; the kernels
+    # its device-side loop ran are the call's iterations (calls with deferred
+    # accumulation run sized launch batches, which the library counts itself)
+    launches += sum(int(p.get("iters") or 0) for p in prof if p.get("graph"))
     elapsed = e0.elapsed_time(e1) / 1e3
     if world > 1:
         t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)

@@ -52,12 +52,15 @@ _GRAPH = [os.environ.get("EK_LEJA_GRAPH", "1") != "0"]
 # Deferred accumulation (ek_leja_run_seq / ek_leja_combine): on large grids the
 # iterations keep every iterate in its own buffer and one pass forms the
 # accumulators at the end — M + 1 + k vector transfers per call instead of
-# 2kM, the same bits. [on, smallest vector length, smallest group, byte budget
-# of the iterate buffers of one call]
+# 2kM, the same bits. [on, smallest vector length, smallest group (analytic
+# Jacobian), byte budget of the iterate buffers of one call, smallest group
+# (FD Jacobian: the K = 0 iteration saves the second f evaluation's traffic
+# too, so a single accumulator already pays: config 4 k = 1 call 5.6 -> 4.9 ms)]
 _DEFER = [os.environ.get("EK_LEJA_DEFER", "1") != "0",
           int(os.environ.get("EK_LEJA_DEFER_MIN_N", str(1 << 22))),
           int(os.environ.get("EK_LEJA_DEFER_MIN_K", "2")),
-          int(os.environ.get("EK_LEJA_DEFER_BYTES", str(48 << 30)))]
+          int(os.environ.get("EK_LEJA_DEFER_BYTES", str(48 << 30))),
+          int(os.environ.get("EK_LEJA_DEFER_MIN_K_FD", "1"))]
 
 
 def generate_leja_points(m=DEFAULT_NUM_POINTS, n_candidates=DEFAULT_CANDIDATES):
@@ -438,7 +441,8 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     fold = Jn is not None and not slab and max_points > 1
     # deferred accumulation: large whole-grid calls (bandwidth-bound); the
     # iterate buffers of one chunk must fit the byte budget
-    da = bool(fold and _DEFER[0] and n >= _DEFER[1] and k >= _DEFER[2]
+    da = bool(fold and _DEFER[0] and n >= _DEFER[1]
+              and k >= (_DEFER[4] if Jn.jac == N.JAC_FD else _DEFER[2])
               and min(_CHUNK, max_points) * n * 8 <= _DEFER[3])
     # graph mode: one graph launch covers the whole first chunk
     graph = fold and _FASTCALL and _GRAPH[0] and not da
@@ -531,7 +535,7 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
     prof = None
     if PROFILE is not None and Jn is not None:
         prof = {"events": [], "k": k, "n": n, "fd": Jn.jac == N.JAC_FD, "deferred": da,
-                "launches": [], "combine_events": []}
+                "graph": bool(graph), "launches": [], "combine_events": []}
         PROFILE.append(prof)
     while m < max_points:
         if m >= m_avail:  # next 32-point chunk (leja.py:168-171)

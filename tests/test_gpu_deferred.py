@@ -30,6 +30,7 @@ def _mode(on):
     L._DEFER[0] = on
     L._DEFER[1] = 0   # any vector length
     L._DEFER[2] = 1   # any group size
+    L._DEFER[4] = 1
 
 
 def _setup(name, n, analytic):

@@ -47,7 +47,7 @@ def main():
 
     if args.defer is not None:
         L._DEFER[0] = bool(args.defer)
-        L._DEFER[1], L._DEFER[2] = 0, 1
+        L._DEFER[1], L._DEFER[2], L._DEFER[4] = 0, 1, 1
     prob = ext.make_ext_problem(args.problem, n=args.n)
     rhs = ek.CountingRhs(prob.rhs)
     sys_ = ek.make_linearized(rhs, prob.u0, jac_factory=prob.jac_factory)
