@@ -231,3 +231,29 @@ def test_batched_divided_differences_bit_identical():
         hs = [ci * dt for ci in sorted(rng.uniform(0.05, 1.0, int(rng.integers(1, 4))))]
         for h, d in zip(hs, phi_divided_differences_many(l, hs, c, g, xi, m)):
             assert np.array_equal(d, phi_divided_differences(l, h, c, g, xi, m))
+
+
+def test_bench_byte_models_of_the_leja_call():
+    """bench.py's roofline bytes: per-iteration accumulation counts the live
+    accumulators of every iteration; the deferred form
+    counts k = 0 iterations plus one combine pass of M + 1 + k vectors."""
+    import importlib.util
+    from pathlib import Path
+    spec = importlib.util.spec_from_file_location(
+        "bench_root", Path(__file__).resolve().parents[1] / "bench.py")
+    B = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B)
+    n = 1000
+    prof = {"n": n, "fd": True, "k": 3, "iters": 4, "freeze": [2, 4, 4]}
+    alg, pas, launches = B.leja_bytes(prof)
+    # live accumulators per iteration: 3, 3, 2, 2
+    assert launches == 4
+    assert alg == 8 * n * (4 * 4 + 2 * (3 + 3 + 2 + 2))
+    assert pas == 8 * n * (3 * 4 + 2 * (3 + 3 + 2 + 2))
+    assert B.combine_bytes(prof) == 0
+    prof["deferred"] = True
+    alg, pas, launches = B.leja_bytes(prof)
+    assert alg == pas == 8 * n * 4 * 4 and launches == 4
+    assert B.combine_bytes(prof) == 8 * n * (4 + 1 + 3)
+    lin = {"n": n, "fd": False, "k": 2, "iters": 3, "freeze": [3, 3], "deferred": True}
+    assert B.leja_bytes(lin)[0] == 8 * n * 2 * 3
