@@ -50,6 +50,8 @@ CALLS = [("advdiff2d", 128, True, 20.0, [0.5, 1.0]),
          ("advdiff3d", 34, True, 20.0, [0.5, 1.0]),
          ("advdiff3d", 70, True, 40.0, [0.25, 1.0]),
          ("advdiff2d", 128, True, 400.0, [0.5, 1.0]),   # crosses 32-point chunks
+         ("brusselator_periodic", 96, False, 400.0, [0.3, 0.7, 1.0]),   # FD, crosses chunks
+         ("advdiff3d", 40, True, 400.0, [0.5, 1.0]),    # 3-D, crosses chunks
          ("advdiff2d", 128, True, 1e-6, [0.5, 1.0])]    # everything freezes at m = 0
 
 
