@@ -60,19 +60,33 @@ constexpr int CTR2 = 256;  // doubles per centre row slot
 // that instance streams the stored f(u_n) as a centre field instead and
 // evaluates f once per point.
 #ifndef EK_FD_READFU
-#define EK_FD_READFU 1
+#define EK_FD_READFU 2  // 0 re-evaluate, 1 staged: 0.1955 ms, 2 direct loads: 0.1935 ms (config 4)
 #endif
 template <int EV, int EP, int K>
 __host__ __device__ constexpr bool march_rfu() {
     return EK_FD_READFU && EV == EV_FD && EP == EP_LEJA && K == 0;
 }
+// EK_FD_READFU = 1: f(u_n) staged as a centre field of the row ring; 2: loaded
+// by the thread that uses it straight from global memory one row ahead (the
+// ring keeps its smaller stage, so more rows are in flight per block).
+__host__ __device__ constexpr bool march_rfu_direct_on() {
+    return EK_FD_READFU == 2 && EK_PROD2 && EK_TIGHT2;
+}
+template <int EV, int EP, int K>
+__host__ __device__ constexpr bool march_rfu_staged() {
+    return march_rfu<EV, EP, K>() && !march_rfu_direct_on();
+}
+template <int EV, int EP, int K>
+__host__ __device__ constexpr bool march_rfu_direct() {
+    return march_rfu<EV, EP, K>() && EK_FD_READFU == 2 && EK_PROD2 && EK_TIGHT2;
+}
 template <int EV, int EP, int K>
 __host__ __device__ constexpr bool march_fu() {
-    return needs_fu<EV>() || march_rfu<EV, EP, K>();
+    return needs_fu<EV>() || march_rfu_staged<EV, EP, K>();
 }
 template <int EV, int EP, int K>
 __host__ __device__ constexpr int nctr2() {
-    return nctr_maps<EV, EP, K>() + (march_rfu<EV, EP, K>() ? 1 : 0);
+    return nctr_maps<EV, EP, K>() + (march_rfu_staged<EV, EP, K>() ? 1 : 0);
 }
 
 template <int EV, int EP, int NC, int K>
@@ -173,7 +187,7 @@ __device__ __forceinline__ void issue_row(const KArgs& a, double* buf, uint64_t*
 #pragma unroll
         for (int g = 0; g < NCM; ++g)
             if (g < FU || ((active >> (g - FU)) & 1u)) {
-                const double* fb = (march_rfu<EV, EP, K>() && g == 0) ? a.fu
+                const double* fb = (march_rfu_staged<EV, EP, K>() && g == 0) ? a.fu
                                                                       : ctr_field<EV, EP>(a, g);
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
@@ -188,7 +202,8 @@ __device__ __forceinline__ void issue_row(const KArgs& a, double* buf, uint64_t*
 template <class P, int EV, int EP, int K, class XS>
 __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, const double* pm,
                                              const double* pc, const double* pp, long i, int j,
-                                             int t, int cols, double* acc, XS xs) {
+                                             int t, int cols, double* acc, XS xs,
+                                             const double* fug = nullptr) {
     constexpr int NC = P::NC, NCH = ev_nch(EV), NR = nraw<EV>();
     constexpr int FU = march_fu<EV, EP, K>() ? 1 : 0;
     Nb nb[NC][NCH];
@@ -219,7 +234,8 @@ __device__ __forceinline__ void march2_point(const KArgs& a, const Ctl& ctl, con
     const double* ctr = pc + NR * NC * RAW2;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-        z.fu[c] = FU ? ctr[c * CTR2 + t] : 0.0;
+        if constexpr (march_rfu_direct<EV, EP, K>()) z.fu[c] = fug[c];
+        else z.fu[c] = FU ? ctr[c * CTR2 + t] : 0.0;
         if constexpr (EP == EP_RHSN) z.y[c] = yc[c];  // u at the centre
         if constexpr (EP == EP_LEJA || EP == EP_ARN) {
             z.y[c] = yc[c];
@@ -356,9 +372,18 @@ __global__ void __launch_bounds__(NT2, (march2_lb<EP, K>())) k_march2d(const KAr
             const double* pc = smem + sc * SD;
             long i = it.r0;
             for (int p = 1; p <= it.L; ++p, ++i) {
+                double fug[NC];
+                if constexpr (march_rfu_direct<EV, EP, K>()) {
+                    // f(u_n) at this thread's point, in flight while the warp
+                    // waits for row i + 1 and evaluates f(u_n + eps y)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        fug[c] = live ? __ldg(a.fu + c * a.npts + i * cols + j) : 0.0;
+                }
                 const int sp = wait_next();
                 const double* pp = smem + sp * SD;
-                if (live) march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs);
+                if (live)
+                    march2_point<P, EV, EP, K>(a, ctl, pm, pc, pp, i, j, t, cols, acc, xs, fug);
                 release_s(sm);
                 sm = sc; sc = sp; pm = pc; pc = pp;
             }
