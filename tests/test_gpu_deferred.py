@@ -167,3 +167,35 @@ def test_fixed_steps_epirk5p1_unchanged_by_deferred_mode(defer_switch):
     (ua, sa, ca), (ud, sd, cd) = runs[False], runs[True]
     assert sd == sa and cd == ca
     assert np.array_equal(ud, ua)
+
+
+def test_deferred_mode_selection(defer_switch):
+    """The form is chosen per call: on by size / group thresholds, off when the
+    chunk's iterate buffers would exceed the byte budget or the switch is
+    off; the profile record says which ran."""
+    xi = ek.get_leja_points(400)
+    p, rhs, sys_, est = _setup("brusselator_periodic", 96, False)
+    dt = 30.0 / abs(est.alpha)
+    b = sys_.f_n * dt
+
+    def ran_deferred():
+        L.PROFILE = []
+        try:
+            ek.leja_interpolate_vertical(sys_.J, b, 1, [0.5, 1.0], dt, est, 1e-10, xi=xi)
+            return L.PROFILE[0]["deferred"]
+        finally:
+            L.PROFILE = None
+
+    _mode(True)
+    assert ran_deferred() is True
+    L._DEFER[3] = 8            # byte budget smaller than one iterate
+    assert ran_deferred() is False
+    _mode(True)
+    L._DEFER[3] = 48 << 30
+    L._DEFER[1] = 1 << 40      # vector length threshold above this grid
+    assert ran_deferred() is False
+    _mode(False)
+    assert ran_deferred() is False
+    _mode(True)
+    L._DEFER[4] = 3            # FD calls need >= 3 coefficients: this one has 2
+    assert ran_deferred() is False
