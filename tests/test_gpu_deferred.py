@@ -199,3 +199,26 @@ def test_deferred_mode_selection(defer_switch):
     _mode(True)
     L._DEFER[4] = 3            # FD calls need >= 3 coefficients: this one has 2
     assert ran_deferred() is False
+
+
+@pytest.mark.parametrize("name,analytic", [("advdiff2d", True), ("brusselator_periodic", False)])
+def test_deferred_call_raises_as_the_per_iteration_form(defer_switch, name, analytic):
+    """A spectrum estimate far too small makes the iteration blow up: both
+    forms stop at the same iteration with the same exception (overflowing
+    norm -> NonConvergence, non-finite FD action -> FloatingPointError;
+    leja.py:174-175, linalg.py:127-128)."""
+    xi = ek.get_leja_points(400)
+    p, rhs, sys_, est = _setup(name, 96, analytic)
+    bad = ek.make_estimate(est.alpha * 1e-4)
+    dt = 30.0 / abs(est.alpha)
+    b = sys_.f_n * dt
+    seen = {}
+    for mode in (False, True):
+        _mode(mode)
+        L._DD_CACHE.clear()
+        c0 = rhs.counter.count
+        with pytest.raises((ek.NonConvergence, FloatingPointError)) as ei:
+            ek.leja_interpolate_vertical(sys_.J, b, 1, [0.5, 1.0], dt, bad, 1e-10, xi=xi)
+        seen[mode] = (type(ei.value), str(ei.value), getattr(ei.value, "iters", None),
+                      rhs.counter.count - c0)
+    assert seen[True] == seen[False]
