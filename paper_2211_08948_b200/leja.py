@@ -55,7 +55,7 @@ _GRAPH = [os.environ.get("EK_LEJA_GRAPH", "1") != "0"]
 # 2kM, the same bits. [on, smallest vector length, smallest group (analytic
 # Jacobian), byte budget of the iterate buffers of one call, smallest group
 # (FD Jacobian: the K = 0 iteration saves the second f evaluation's traffic
-# too, so a single accumulator already pays: config 4 k = 1 call 5.6 -> 4.9 ms)]
+# too, so a single accumulator already pays: config 4 k = 1 call 5.56 -> 5.05 ms)]
 _DEFER = [os.environ.get("EK_LEJA_DEFER", "1") != "0",
           int(os.environ.get("EK_LEJA_DEFER_MIN_N", str(1 << 22))),
           int(os.environ.get("EK_LEJA_DEFER_MIN_K", "2")),
@@ -477,11 +477,20 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
             yout.append(Y[j])
         return N.ptrs(yin), N.ptrs(yout)
 
-    def combine(base_):
+    def combine(base_, timed=True):
+        """Form the sums over the current chunk's iterates (the freeze points
+        are read from the state block on the device)."""
         ny = max(j for j in range(_CHUNK) if Y[j] is not None) + 1
+        cev = None
+        if timed and prof is not None:
+            cev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            cev[0].record()
         N.check(N.lib().ek_leja_combine(
             n, N.ptrs(Y[:ny]), ny, pp, k, C.c_void_p(table.dev.data_ptr()), base_,
             1 if base_ > 0 else 0, st.ptr, D.stream()), "ek_leja_combine")
+        if cev is not None:
+            cev[1].record()
+            prof["combine_events"].append(cev)
 
     if fast and da and not spec_zero:
         yin0, yout0 = seq_buffers(1, first_hi, 0)
@@ -544,7 +553,7 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                 _dd_prefetch(l, ci * h, est, xi, min(m_avail + _CHUNK, max_points))
             dds = [_dd_cached(l, ci * h, est, xi, m_avail) for ci in coeffs]
             if da:  # fold the finished chunk into the sums before its table goes
-                combine(base)
+                combine(base, timed=False)
                 yprev = Y[m - 1 - base]
                 pool.extend(y for j, y in enumerate(Y)
                             if y is not None and y is not yprev and y is not bd)
@@ -608,15 +617,7 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                 ev[1].record()
                 prof["events"].append(ev)
             if spec and da:
-                # the freeze points are read from the state block on the device
-                if prof is not None:
-                    cev = (torch.cuda.Event(enable_timing=True),
-                           torch.cuda.Event(enable_timing=True))
-                    cev[0].record()
                 combine(base)
-                if prof is not None:
-                    cev[1].record()
-                    prof["combine_events"].append(cev)
             if spec:
                 def on_state(hst, prof=prof):
                     if hst.status != N.ST_OK or not hst.done:
@@ -664,14 +665,7 @@ def leja_interpolate_vertical(J: MatrixFreeOperator, b, l, coeffs, h, est, tol,
                 return LejaResult(vectors=[float(dds[i][0]) * D.V(bd) for i in range(k)],
                                   iters=0, freeze_iters=[0] * k)
             if da:
-                if prof is not None:
-                    cev = (torch.cuda.Event(enable_timing=True),
-                           torch.cuda.Event(enable_timing=True))
-                    cev[0].record()
                 combine(base)
-                if prof is not None:
-                    cev[1].record()
-                    prof["combine_events"].append(cev)
             return LejaResult(vectors=[D.like_input(p, b) for p in ps],
                               iters=int(hst.iters),
                               freeze_iters=[int(hst.freeze[i]) for i in range(k)])
